@@ -1,0 +1,192 @@
+/*
+ * adr_splat.h — C ABI of the B200 AdR-Gaussian forward rasterizer
+ * (libadrsplat.so, sm_100a).
+ *
+ * The reference (splatbench 0.1.0, /root/reference/pkg/src/splatbench/) is a
+ * pure-Python package with no FFI.  These entry points are what its Python
+ * stage functions bind to (see INTEGRATION.md for the ctypes stubs); each
+ * cites the reference function it replaces.  Conventions:
+ *
+ *  - every pointer named d_* is DEVICE memory owned by the caller; h_* is host;
+ *  - every call is asynchronous on `stream` (a cudaStream_t passed as void*),
+ *    except the ones documented as synchronising;
+ *  - scratch memory is caller-provided: call the matching *_scratch_bytes()
+ *    first (cub-style two-phase API); the library never allocates device
+ *    memory itself;
+ *  - return value is an adr_status; adr_last_error() gives the message.
+ *    ADR_ERR_VALUE maps to ValueError, ADR_ERR_CAPACITY to CapacityError,
+ *    ADR_ERR_INTERNAL to InternalError (sb/errors.py:4-17).
+ */
+#ifndef ADR_SPLAT_H
+#define ADR_SPLAT_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define ADR_ABI_VERSION 1
+
+typedef enum {
+    ADR_OK = 0,
+    ADR_ERR_VALUE = 1,     /* bad argument            -> ValueError    */
+    ADR_ERR_CAPACITY = 2,  /* key / index overflow    -> CapacityError */
+    ADR_ERR_INTERNAL = 3,  /* invariant violated      -> InternalError */
+    ADR_ERR_CUDA = 4       /* CUDA runtime failure    -> RuntimeError  */
+} adr_status;
+
+/* CullingMode (sb/projection.py:46-49). */
+typedef enum { ADR_MODE_BASELINE = 0, ADR_MODE_CIRCLE = 1, ADR_MODE_AABB = 2 } adr_mode;
+
+/* Scene storage dtype. Math is fp64 either way (bit-exact with the reference
+ * when the stored values are the reference's values). */
+typedef enum { ADR_F32 = 0, ADR_F64 = 1 } adr_dtype;
+
+/* Camera constants, computed on the host with the reference's own
+ * expressions (sb/projection.py:341-355, sb/scene.py:147-158). */
+typedef struct {
+    double rot[9];        /* world->camera rotation, row-major */
+    double trans[3];
+    double center[3];     /* -R^T t */
+    double fx, fy;
+    double lim_x, lim_y;  /* FOV_CLAMP_FACTOR * (0.5 * W / f) */
+    double cx, cy;        /* 0.5 * (W - 1), 0.5 * (H - 1) */
+    double near_plane;
+    float background[3];
+    int32_t width, height;
+} adr_camera;
+
+/* Scene arrays (SceneArrays, sb/scene.py:105-110), device, row-major:
+ * centers (N,3), scales (N,3), rotations (N,4) wxyz, opacities (N,),
+ * sh (N,K,3) with K = (sh_degree+1)^2. */
+typedef struct {
+    const void* d_centers;
+    const void* d_scales;
+    const void* d_rotations;
+    const void* d_opacities;
+    const void* d_sh;
+    int64_t n;
+    int32_t sh_degree;
+    int32_t dtype;        /* adr_dtype */
+} adr_scene;
+
+/* Projection (sb/projection.py:86-112), device, index-aligned with the scene. */
+typedef struct {
+    uint8_t* d_valid;       /* (N,)   bool  */
+    float* d_mean2d;        /* (N,2)        */
+    float* d_cov2d;         /* (N,3)  sxx, syy, sxy */
+    float* d_conic;         /* (N,3)  a, b, c       */
+    float* d_depth;         /* (N,)         */
+    float* d_color;         /* (N,3)        */
+    float* d_opacity;       /* (N,)         */
+    float* d_lambda_max;    /* (N,)         */
+    int32_t* d_ext_x;       /* (N,)         */
+    int32_t* d_ext_y;       /* (N,)         */
+} adr_projection;
+
+/* ---------------------------------------------------------------- utils */
+int32_t adr_abi_version(void);
+const char* adr_last_error(void);
+/* Running total of kernels this library has launched (all entry points). */
+int64_t adr_kernel_launches(void);
+/* Number of SMs of the current device (for diagnostics). */
+int32_t adr_device_sm_count(void);
+
+/* ------------------------------------------------------- stage functions */
+
+/* Stage 1 — preprocess (sb/projection.py:291-420). Writes every Projection
+ * field; rows that do not survive are zeroed (valid = 0). */
+int32_t adr_preprocess(const adr_scene* scene, const adr_camera* cam, int32_t mode,
+                       double alpha_low, double dilation, const adr_projection* out,
+                       void* stream);
+
+/* Stage 2a — touched-tile counts (sb/tiling.py:111-114, rects :77-99). */
+int32_t adr_touched_counts(const adr_projection* proj, int64_t n, int32_t tiles_x,
+                           int32_t tiles_y, int64_t* d_counts, void* stream);
+
+/* Stage 2b — inclusive sum (sb/tiling.py:117-122), int64.  The overflow
+ * check of the reference becomes a device flag: *d_overflow is set to 1 when
+ * the running sum exceeds INT64_MAX (caller maps it to CapacityError). */
+size_t adr_inclusive_sum_scratch_bytes(int64_t n);
+int32_t adr_inclusive_sum(const int64_t* d_counts, int64_t n, int64_t* d_offsets,
+                          int32_t* d_overflow, void* d_scratch, size_t scratch_bytes,
+                          void* stream);
+
+/* Stage 3 — duplicate with keys (sb/tiling.py:125-156): entries of Gaussian g
+ * fill [offsets[g]-count, offsets[g]) row-major over its tile rectangle,
+ * key = tile << 32 | float32 depth bits, gidx = g. */
+int32_t adr_duplicate_with_keys(const adr_projection* proj, int64_t n,
+                                const int64_t* d_offsets, int32_t tiles_x, int32_t tiles_y,
+                                uint64_t* d_keys, int64_t* d_gidx, void* stream);
+
+/* Stage 4 — stable ascending sort by key (sb/tiling.py:159-164): LSD radix
+ * sort over bits [0, end_bit) (end_bit <= 64; pass 64 for arbitrary keys).
+ * Inputs are not modified. */
+size_t adr_sort_pairs_scratch_bytes(int64_t p);
+int32_t adr_sort_pairs(const uint64_t* d_keys, const int64_t* d_gidx, int64_t p,
+                       int32_t end_bit, uint64_t* d_keys_out, int64_t* d_gidx_out,
+                       void* d_scratch, size_t scratch_bytes, void* stream);
+
+/* Stage 5 — tile ranges (sb/tiling.py:167-177): ranges (n_tiles,2) int64,
+ * empty tiles (k,k).  *d_error gets 1 if keys are unsorted, 2 if a key
+ * references a tile >= n_tiles (caller maps both to InternalError). */
+int32_t adr_identify_tile_ranges(const uint64_t* d_sorted_keys, int64_t p, int64_t n_tiles,
+                                 int64_t* d_ranges, int32_t* d_error, void* stream);
+
+/* Load-map statistics produced by the render epilogue (LoadStats,
+ * sb/metrics.py:59-86): exact integer moments, min, max.  The histogram is
+ * optional (d_hist may be NULL); when given it has hist_bins entries and
+ * counts >= hist_bins are clamped into the last bin. */
+typedef struct {
+    int64_t sum;
+    int64_t sum_sq;
+    int32_t min;
+    int32_t max;
+} adr_load_stats;
+
+/* Stage 6 — render (sb/render.py:128-171): per-tile front-to-back blend and
+ * per-pixel composited count.  d_gidx lists, per sorted pair, the Gaussian
+ * index into the projection; d_ranges is the (n_tiles,2) span table. */
+int32_t adr_render(const adr_projection* proj, int64_t n, const int64_t* d_gidx, int64_t p,
+                   const int64_t* d_ranges, const adr_camera* cam, double alpha_low,
+                   double term_threshold, float* d_pixels, int32_t* d_counts,
+                   adr_load_stats* d_stats, int32_t* d_hist, int32_t hist_bins, void* stream);
+
+/* --------------------------------------------- fused pipeline (run_pipeline)
+ * sb/pipeline.py:85-124.  The frame runs as a fixed kernel sequence with no
+ * host synchronisation, so it can be captured into a CUDA graph.  Pair
+ * buffers have a caller-chosen capacity; when the frame needs more pairs the
+ * frame still completes (no out-of-bounds writes), *d_pair_count holds the
+ * true P and the caller re-runs with a larger capacity.
+ */
+typedef struct {
+    /* outputs (device) */
+    adr_projection proj;          /* Projection                           */
+    float* d_pixels;              /* (H,W,3)                              */
+    int32_t* d_load;              /* (H,W)                                */
+    uint64_t* d_keys;             /* (pair_capacity,) sorted keys (opt.)   */
+    int32_t* d_gidx;              /* (pair_capacity,) sorted gidx (opt.)   */
+    int64_t* d_ranges;            /* (n_tiles,2)                           */
+    int64_t* d_counters;          /* [0]=P, [1]=culled, [2]=M (Gaussians with pairs) */
+    adr_load_stats* d_stats;
+    int32_t* d_hist;              /* optional, hist_bins entries           */
+    int32_t hist_bins;
+    /* workspace */
+    void* d_scratch;
+    size_t scratch_bytes;
+    int64_t pair_capacity;
+    /* optional per-stage CUDA events (7 cudaEvent_t as void*), may be NULL */
+    void* const* events;
+} adr_frame_buffers;
+
+size_t adr_frame_scratch_bytes(int64_t n, int32_t width, int32_t height, int64_t pair_capacity);
+int32_t adr_render_frame(const adr_scene* scene, const adr_camera* cam, int32_t mode,
+                         double alpha_low, double dilation, double term_threshold,
+                         const adr_frame_buffers* buf, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif

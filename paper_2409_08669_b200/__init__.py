@@ -1,0 +1,33 @@
+"""B200-native AdR-Gaussian forward rasterizer (arXiv 2409.08669).
+
+Drop-in for the reference package's render API (splatbench 0.1.0,
+sb/__init__.py:10-48): the same stage functions, containers, constants and
+exceptions, backed by hand-written sm_100a kernels in libadrsplat.so
+(include/adr_splat.h).  Arrays are CUDA tensors; each container has
+``to_numpy()`` for the reference's numpy layout.
+"""
+
+from .errors import CapacityError, InternalError, SceneFormatError, SceneValidationError
+from .metrics import PSNR_IDENTICAL_SENTINEL, LoadStats, load_loss, psnr
+from .pipeline import STAGE_NAMES, PipelineResult, Rasterizer, RenderStats, run_pipeline
+from .projection import (ALPHA_LOW, BASE_RADIUS_MULTIPLIER, COV_DILATION, FOV_CLAMP_FACTOR,
+                         CullingMode, Projection, preprocess)
+from .render import ALPHA_CLAMP, TERMINATION_THRESHOLD, Image, LoadMap, render
+from .scene import (Camera, DeviceScene, Gaussian3D, Scene, SceneArrays, SyntheticSpec,
+                    generate_synthetic, synthetic_arrays)
+from .tiling import (TILE_SIZE, TileGrid, TilePairList, TileRect, build_pairs,
+                     duplicate_with_keys, identify_tile_ranges, inclusive_sum, sort_pairs,
+                     tiles_touched, touched_counts)
+
+__version__ = "0.1.0"
+
+__all__ = [
+    "ALPHA_CLAMP", "ALPHA_LOW", "BASE_RADIUS_MULTIPLIER", "COV_DILATION", "FOV_CLAMP_FACTOR",
+    "PSNR_IDENTICAL_SENTINEL", "STAGE_NAMES", "TERMINATION_THRESHOLD", "TILE_SIZE", "Camera",
+    "CapacityError", "CullingMode", "DeviceScene", "Gaussian3D", "Image", "InternalError",
+    "LoadMap", "LoadStats", "PipelineResult", "Projection", "Rasterizer", "RenderStats", "Scene",
+    "SceneArrays", "SceneFormatError", "SceneValidationError", "SyntheticSpec", "TileGrid",
+    "TilePairList", "TileRect", "build_pairs", "duplicate_with_keys", "generate_synthetic",
+    "identify_tile_ranges", "inclusive_sum", "load_loss", "preprocess", "psnr", "render",
+    "run_pipeline", "sort_pairs", "synthetic_arrays", "tiles_touched", "touched_counts",
+]

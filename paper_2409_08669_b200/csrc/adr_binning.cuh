@@ -1,0 +1,46 @@
+// adr_binning.cuh — stages 2-5 launchers (stage API + fused frame).
+#pragma once
+
+#include "adr_kernels.cuh"
+
+namespace adr {
+
+int32_t stage_touched_counts(const adr_projection& p, int64_t n, int32_t tx, int32_t ty, int64_t* counts,
+                             cudaStream_t st);
+size_t stage_inclusive_sum_scratch(int64_t n);
+int32_t stage_inclusive_sum(const int64_t* in, int64_t n, int64_t* out, int32_t* overflow, void* scratch,
+                            size_t bytes, cudaStream_t st);
+int32_t stage_duplicate(const adr_projection& p, int64_t n, const int64_t* offsets, int32_t tx, int32_t ty,
+                        uint64_t* keys, int64_t* gidx, cudaStream_t st);
+size_t stage_sort_scratch(int64_t p);
+int32_t stage_sort(const uint64_t* k, const int64_t* v, int64_t p, int32_t end_bit, uint64_t* ko, int64_t* vo,
+                   void* scratch, size_t bytes, cudaStream_t st);
+int32_t stage_ranges(const uint64_t* keys, int64_t p, int64_t n_tiles, int64_t* ranges, int32_t* error,
+                     cudaStream_t st);
+
+// Fused-frame binning: compaction → depth-rank sort of Gaussians → rank-ordered
+// pair emission → stable tile sort → ranges (→ optional reference-layout export).
+struct FrameBinning {
+    adr_projection proj;
+    int64_t n = 0;
+    int64_t cap = 0;            // pair capacity
+    int64_t n_tiles = 0;
+    int32_t tiles_x = 0, tiles_y = 0;
+    uint32_t* cnt = nullptr;    // per-Gaussian touched counts (from stage 1)
+    uint32_t* order = nullptr;  // out: order[rank] = Gaussian index
+    Record* rec = nullptr;      // out: records by rank
+    uint32_t* sorted_ranks = nullptr;  // out: per sorted pair, rank
+    int64_t* ranges = nullptr;  // out: (n_tiles, 2)
+    uint64_t* keys = nullptr;   // optional export
+    int32_t* gidx = nullptr;    // optional export
+    int64_t* counters = nullptr;
+    void* scratch = nullptr;
+    size_t scratch_bytes = 0;
+    cudaEvent_t ev_after_scan = nullptr, ev_after_dup = nullptr, ev_after_sort = nullptr,
+                ev_after_ranges = nullptr;
+};
+
+size_t frame_binning_scratch(int64_t n, int64_t cap, int64_t n_tiles);
+int32_t frame_binning(const FrameBinning& fb, cudaStream_t st);
+
+}  // namespace adr

@@ -1,0 +1,257 @@
+// adr_preprocess.cu — stage 1 (sb/projection.py:291-420), one thread per
+// Gaussian, fp64 math in the reference's evaluation order.
+//
+// Bit-exactness notes:
+//  * numpy elementwise ops → one IEEE op each (explicit __d*_rn intrinsics);
+//  * p_view = centers @ R.T + t and cov3d = m @ m^T → OpenBLAS dgemm order
+//    fma(c2,R2, fma(c1,R1, c0*R0)) (+ t);
+//  * c_t = cov3d @ t (batched dgemv) → fma(cov2,t2, fma(cov0,t0, cov1*t1));
+//  * np.sum over 3 terms → (a+b)+c; outputs rounded fp64→fp32 (RN).
+#include "adr_kernels.cuh"
+#include "adr_scan.cuh"
+
+namespace adr {
+
+namespace {
+
+__device__ __constant__ double kShC0 = 0.28209479177387814;
+__device__ __constant__ double kShC1 = 0.4886025119029199;
+__device__ __constant__ double kShC2[5] = {1.0925484305920792, -1.0925484305920792, 0.31539156525252005,
+                                           -1.0925484305920792, 0.5462742152960396};
+__device__ __constant__ double kShC3[7] = {-0.5900435899266435, 2.890611442640554, -0.4570457994644658,
+                                           0.3731763325901154, -0.4570457994644658, 1.445305721320277,
+                                           -0.5900435899266435};
+
+#define MUL __dmul_rn
+#define ADD __dadd_rn
+#define SUB __dsub_rn
+#define FMA __fma_rn
+
+// sb/projection.py:140-163 for one channel (Python left-to-right order).
+template <int DEG>
+__device__ __forceinline__ double sh_channel(const double* c, double x, double y, double z) {
+    double r = MUL(kShC0, c[0]);
+    if (DEG > 0) {
+        r = SUB(ADD(SUB(r, MUL(MUL(kShC1, y), c[1])), MUL(MUL(kShC1, z), c[2])), MUL(MUL(kShC1, x), c[3]));
+    }
+    if (DEG > 1) {
+        const double xx = MUL(x, x), yy = MUL(y, y), zz = MUL(z, z);
+        const double xy = MUL(x, y), yz = MUL(y, z), xz = MUL(x, z);
+        r = ADD(r, MUL(MUL(kShC2[0], xy), c[4]));
+        r = ADD(r, MUL(MUL(kShC2[1], yz), c[5]));
+        r = ADD(r, MUL(MUL(kShC2[2], SUB(SUB(MUL(2.0, zz), xx), yy)), c[6]));
+        r = ADD(r, MUL(MUL(kShC2[3], xz), c[7]));
+        r = ADD(r, MUL(MUL(kShC2[4], SUB(xx, yy)), c[8]));
+        if (DEG > 2) {
+            r = ADD(r, MUL(MUL(MUL(kShC3[0], y), SUB(MUL(3.0, xx), yy)), c[9]));
+            r = ADD(r, MUL(MUL(MUL(kShC3[1], xy), z), c[10]));
+            r = ADD(r, MUL(MUL(MUL(kShC3[2], y), SUB(SUB(MUL(4.0, zz), xx), yy)), c[11]));
+            r = ADD(r, MUL(MUL(MUL(kShC3[3], z), SUB(SUB(MUL(2.0, zz), MUL(3.0, xx)), MUL(3.0, yy))), c[12]));
+            r = ADD(r, MUL(MUL(MUL(kShC3[4], x), SUB(SUB(MUL(4.0, zz), xx), yy)), c[13]));
+            r = ADD(r, MUL(MUL(MUL(kShC3[5], z), SUB(xx, yy)), c[14]));
+            r = ADD(r, MUL(MUL(MUL(kShC3[6], x), SUB(xx, MUL(3.0, yy))), c[15]));
+        }
+    }
+    return np_clip(ADD(r, 0.5), 0.0, 1.0);
+}
+
+template <typename T, int DEG, bool FUSED>
+__global__ void __launch_bounds__(128)
+k_preprocess(const T* __restrict__ centers, const T* __restrict__ scales,
+             const T* __restrict__ rotations, const T* __restrict__ opacities,
+             const T* __restrict__ sh, int64_t n, adr_camera cam, int32_t mode,
+             double alpha_low, double dilation, adr_projection out, FusedPre fused) {
+    constexpr int K = (DEG + 1) * (DEG + 1);
+    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    bool alive = false;
+    if (i < n) {
+        const double* R = cam.rot;
+        const double c0 = (double)centers[3 * i], c1 = (double)centers[3 * i + 1],
+                     c2 = (double)centers[3 * i + 2];
+        double pv[3];
+#pragma unroll
+        for (int k = 0; k < 3; ++k)
+            pv[k] = ADD(FMA(c2, R[3 * k + 2], FMA(c1, R[3 * k + 1], MUL(c0, R[3 * k + 0]))), cam.trans[k]);
+        const double depth = pv[2];
+        alive = depth > cam.near_plane;
+
+        const double w = (double)rotations[4 * i], x = (double)rotations[4 * i + 1],
+                     y = (double)rotations[4 * i + 2], z = (double)rotations[4 * i + 3];
+        double rq[9];
+        rq[0] = SUB(1.0, MUL(2.0, ADD(MUL(y, y), MUL(z, z))));
+        rq[1] = MUL(2.0, SUB(MUL(x, y), MUL(w, z)));
+        rq[2] = MUL(2.0, ADD(MUL(x, z), MUL(w, y)));
+        rq[3] = MUL(2.0, ADD(MUL(x, y), MUL(w, z)));
+        rq[4] = SUB(1.0, MUL(2.0, ADD(MUL(x, x), MUL(z, z))));
+        rq[5] = MUL(2.0, SUB(MUL(y, z), MUL(w, x)));
+        rq[6] = MUL(2.0, SUB(MUL(x, z), MUL(w, y)));
+        rq[7] = MUL(2.0, ADD(MUL(y, z), MUL(w, x)));
+        rq[8] = SUB(1.0, MUL(2.0, ADD(MUL(x, x), MUL(y, y))));
+        const double s0 = (double)scales[3 * i], s1 = (double)scales[3 * i + 1], s2 = (double)scales[3 * i + 2];
+        double m[9];
+#pragma unroll
+        for (int a = 0; a < 3; ++a) {
+            m[3 * a + 0] = MUL(rq[3 * a + 0], s0);
+            m[3 * a + 1] = MUL(rq[3 * a + 1], s1);
+            m[3 * a + 2] = MUL(rq[3 * a + 2], s2);
+        }
+        double cov[9];
+#pragma unroll
+        for (int a = 0; a < 3; ++a)
+#pragma unroll
+            for (int b = 0; b < 3; ++b)
+                cov[3 * a + b] = FMA(m[3 * a + 2], m[3 * b + 2], FMA(m[3 * a + 1], m[3 * b + 1], MUL(m[3 * a], m[3 * b])));
+
+        const double safe_z = alive ? depth : 1.0;
+        const double inv_z = __ddiv_rn(1.0, safe_z);
+        const double tx = MUL(np_clip(MUL(pv[0], inv_z), -cam.lim_x, cam.lim_x), safe_z);
+        const double ty = MUL(np_clip(MUL(pv[1], inv_z), -cam.lim_y, cam.lim_y), safe_z);
+        const double j0 = MUL(cam.fx, inv_z);
+        const double j2x = MUL(MUL(MUL(-cam.fx, tx), inv_z), inv_z);
+        const double j1 = MUL(cam.fy, inv_z);
+        const double j2y = MUL(MUL(MUL(-cam.fy, ty), inv_z), inv_z);
+        double t0[3], t1[3];
+#pragma unroll
+        for (int k = 0; k < 3; ++k) {
+            t0[k] = ADD(MUL(j0, R[k]), MUL(j2x, R[6 + k]));
+            t1[k] = ADD(MUL(j1, R[3 + k]), MUL(j2y, R[6 + k]));
+        }
+        double ct0[3], ct1[3];
+#pragma unroll
+        for (int a = 0; a < 3; ++a) {
+            ct0[a] = FMA(cov[3 * a + 2], t0[2], FMA(cov[3 * a + 0], t0[0], MUL(cov[3 * a + 1], t0[1])));
+            ct1[a] = FMA(cov[3 * a + 2], t1[2], FMA(cov[3 * a + 0], t1[0], MUL(cov[3 * a + 1], t1[1])));
+        }
+        const double sxx = ADD(ADD(ADD(MUL(t0[0], ct0[0]), MUL(t0[1], ct0[1])), MUL(t0[2], ct0[2])), dilation);
+        const double syy = ADD(ADD(ADD(MUL(t1[0], ct1[0]), MUL(t1[1], ct1[1])), MUL(t1[2], ct1[2])), dilation);
+        const double sxy = ADD(ADD(MUL(t0[0], ct1[0]), MUL(t0[1], ct1[1])), MUL(t0[2], ct1[2]));
+
+        const double det = SUB(MUL(sxx, syy), MUL(sxy, sxy));
+        const double mid = MUL(0.5, ADD(sxx, syy));
+        const double disc = __dsqrt_rn(np_max(SUB(MUL(mid, mid), det), 0.0));
+        const double lam_max = ADD(mid, disc);
+        const double mx = ADD(MUL(MUL(cam.fx, pv[0]), inv_z), cam.cx);
+        const double my = ADD(MUL(MUL(cam.fy, pv[1]), inv_z), cam.cy);
+        const double r_o_real = MUL(3.0, __dsqrt_rn(np_max(lam_max, 0.0)));
+        const double sigma = (double)opacities[i];
+        double ex, ey;
+        if (mode == ADR_MODE_BASELINE) {
+            ex = ceil(r_o_real);
+            ey = ex;
+        } else {
+            alive = alive && (sigma > alpha_low);
+            const double log_ratio = log_fd(np_max(__ddiv_rn(sigma, alpha_low), 1e-300));
+            if (mode == ADR_MODE_CIRCLE) {
+                ex = ceil(np_min(__dsqrt_rn(MUL(MUL(2.0, lam_max), log_ratio)), r_o_real));
+                ey = ex;
+            } else {
+                ex = ceil(np_min(__dsqrt_rn(MUL(MUL(2.0, sxx), log_ratio)), r_o_real));
+                ey = ceil(np_min(__dsqrt_rn(MUL(MUL(2.0, syy), log_ratio)), r_o_real));
+            }
+        }
+        alive = alive && (ex >= 1.0) && (ey >= 1.0);
+
+        out.d_valid[i] = (uint8_t)alive;
+        if (alive) {
+            double d0 = SUB(c0, cam.center[0]), d1 = SUB(c1, cam.center[1]), d2 = SUB(c2, cam.center[2]);
+            const double nrm = __dsqrt_rn(ADD(ADD(MUL(d0, d0), MUL(d1, d1)), MUL(d2, d2)));
+            const double dn = nrm > 0 ? nrm : 1.0;
+            d0 = __ddiv_rn(d0, dn);
+            d1 = __ddiv_rn(d1, dn);
+            d2 = __ddiv_rn(d2, dn);
+            const T* shp = sh + i * (K * 3);
+            double col[3];
+#pragma unroll
+            for (int ch = 0; ch < 3; ++ch) {
+                double cf[K];
+#pragma unroll
+                for (int k = 0; k < K; ++k) cf[k] = (double)shp[k * 3 + ch];
+                col[ch] = sh_channel<DEG>(cf, d0, d1, d2);
+            }
+            const float2 m2 = make_float2(__double2float_rn(mx), __double2float_rn(my));
+            reinterpret_cast<float2*>(out.d_mean2d)[i] = m2;
+            out.d_cov2d[3 * i] = __double2float_rn(sxx);
+            out.d_cov2d[3 * i + 1] = __double2float_rn(syy);
+            out.d_cov2d[3 * i + 2] = __double2float_rn(sxy);
+            out.d_conic[3 * i] = __double2float_rn(__ddiv_rn(syy, det));
+            out.d_conic[3 * i + 1] = __double2float_rn(__ddiv_rn(-sxy, det));
+            out.d_conic[3 * i + 2] = __double2float_rn(__ddiv_rn(sxx, det));
+            out.d_depth[i] = __double2float_rn(depth);
+            out.d_color[3 * i] = __double2float_rn(col[0]);
+            out.d_color[3 * i + 1] = __double2float_rn(col[1]);
+            out.d_color[3 * i + 2] = __double2float_rn(col[2]);
+            out.d_opacity[i] = __double2float_rn(sigma);
+            out.d_lambda_max[i] = __double2float_rn(lam_max);
+            out.d_ext_x[i] = (int32_t)ex;
+            out.d_ext_y[i] = (int32_t)ey;
+            if (FUSED) {
+                const Rect r = tile_rect(m2.x, m2.y, (int32_t)ex, (int32_t)ey, true, fused.tiles_x, fused.tiles_y);
+                const int64_t c = r.count();
+                fused.cnt[i] = (uint32_t)(c < 0xffffffffll ? c : 0xffffffffll);
+            }
+        } else {
+            reinterpret_cast<float2*>(out.d_mean2d)[i] = make_float2(0.f, 0.f);
+            out.d_cov2d[3 * i] = out.d_cov2d[3 * i + 1] = out.d_cov2d[3 * i + 2] = 0.f;
+            out.d_conic[3 * i] = out.d_conic[3 * i + 1] = out.d_conic[3 * i + 2] = 0.f;
+            out.d_depth[i] = 0.f;
+            out.d_color[3 * i] = out.d_color[3 * i + 1] = out.d_color[3 * i + 2] = 0.f;
+            out.d_opacity[i] = 0.f;
+            out.d_lambda_max[i] = 0.f;
+            out.d_ext_x[i] = 0;
+            out.d_ext_y[i] = 0;
+            if (FUSED) fused.cnt[i] = 0;
+        }
+    }
+    if (FUSED) {
+        const uint32_t culled = __ballot_sync(kFull, i < n && !alive);
+        if ((threadIdx.x & 31) == 0 && culled) atomicAdd(fused.culled, (unsigned long long)__popc(culled));
+    }
+}
+
+#undef MUL
+#undef ADD
+#undef SUB
+#undef FMA
+
+template <typename T, bool FUSED>
+int32_t launch_typed(const adr_scene& s, const adr_camera& cam, int32_t mode, double alpha_low,
+                     double dilation, const adr_projection& out, const FusedPre& f, cudaStream_t st) {
+    const int block = 128;
+    const int64_t grid = ceil_div(s.n, block);
+    const T* c = static_cast<const T*>(s.d_centers);
+    const T* sc = static_cast<const T*>(s.d_scales);
+    const T* r = static_cast<const T*>(s.d_rotations);
+    const T* o = static_cast<const T*>(s.d_opacities);
+    const T* sh = static_cast<const T*>(s.d_sh);
+    switch (s.sh_degree) {
+        case 0: k_preprocess<T, 0, FUSED><<<grid, block, 0, st>>>(c, sc, r, o, sh, s.n, cam, mode, alpha_low, dilation, out, f); break;
+        case 1: k_preprocess<T, 1, FUSED><<<grid, block, 0, st>>>(c, sc, r, o, sh, s.n, cam, mode, alpha_low, dilation, out, f); break;
+        case 2: k_preprocess<T, 2, FUSED><<<grid, block, 0, st>>>(c, sc, r, o, sh, s.n, cam, mode, alpha_low, dilation, out, f); break;
+        case 3: k_preprocess<T, 3, FUSED><<<grid, block, 0, st>>>(c, sc, r, o, sh, s.n, cam, mode, alpha_low, dilation, out, f); break;
+        default: return fail(ADR_ERR_VALUE, "sh_degree must be in 0..3");
+    }
+    ADR_LAUNCH_CHECK();
+    return ADR_OK;
+}
+
+}  // namespace
+
+int32_t launch_preprocess(const adr_scene& scene, const adr_camera& cam, int32_t mode,
+                          double alpha_low, double dilation, const adr_projection& out,
+                          const FusedPre* fused, cudaStream_t st) {
+    if (!(alpha_low > 0.0 && alpha_low < 1.0)) return fail(ADR_ERR_VALUE, "alpha_low must lie in (0, 1)");
+    if (!(dilation >= 0.0)) return fail(ADR_ERR_VALUE, "dilation must be non-negative");
+    if (mode < ADR_MODE_BASELINE || mode > ADR_MODE_AABB) return fail(ADR_ERR_VALUE, "unknown culling mode");
+    if (scene.n < 0) return fail(ADR_ERR_VALUE, "negative Gaussian count");
+    if (scene.n == 0) return ADR_OK;
+    FusedPre f = fused ? *fused : FusedPre{};
+    if (scene.dtype == ADR_F32)
+        return fused ? launch_typed<float, true>(scene, cam, mode, alpha_low, dilation, out, f, st)
+                     : launch_typed<float, false>(scene, cam, mode, alpha_low, dilation, out, f, st);
+    if (scene.dtype == ADR_F64)
+        return fused ? launch_typed<double, true>(scene, cam, mode, alpha_low, dilation, out, f, st)
+                     : launch_typed<double, false>(scene, cam, mode, alpha_low, dilation, out, f, st);
+    return fail(ADR_ERR_VALUE, "scene dtype must be ADR_F32 or ADR_F64");
+}
+
+}  // namespace adr
