@@ -260,7 +260,7 @@ def run_ours(args, cfg, rank, world, local):
     for cam in mine:   # size the pair buffers for every view, collect stage times
         res = rast.render(ds, cam, mode=cfg["mode"])
         pairs.append(res.stats.pair_count)
-    rast._ensure_capacity(int(max(pairs) * 1.02) + 1024)
+    rast.fit_capacity(max(pairs))
     for _ in range(3):
         res = rast.render(ds, mine[0], mode=cfg["mode"])
         stage_ms.append({k: v * 1e3 for k, v in res.stats.stage_seconds().items()})

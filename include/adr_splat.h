@@ -166,8 +166,8 @@ typedef struct {
     adr_projection proj;          /* Projection                           */
     float* d_pixels;              /* (H,W,3)                              */
     int32_t* d_load;              /* (H,W)                                */
-    uint64_t* d_keys;             /* (pair_capacity,) sorted keys (opt.)   */
-    int32_t* d_gidx;              /* (pair_capacity,) sorted gidx (opt.)   */
+    uint64_t* d_keys;             /* (pair_capacity,) sorted keys, optional */
+    int32_t* d_gidx;              /* (pair_capacity,) sorted Gaussian indices (required) */
     int64_t* d_ranges;            /* (n_tiles,2)                           */
     int64_t* d_counters;          /* [0]=P, [1]=culled, [2]=M (Gaussians with pairs) */
     adr_load_stats* d_stats;

@@ -261,158 +261,212 @@ struct SelectOp {
     __device__ void total(uint64_t t) const { *d_m = (int64_t)t; }
 };
 
-// Pair offsets in depth-rank order: off[r] = sum_{r' < r} cnt[order[r']].
+// Pair offsets in depth-rank order: off[r] = sum_{r' < r} cnt_r[r'], clamped
+// to the pair capacity; off[M] = min(P, cap) closes the table.
 struct OffsetsOp {
-    const uint32_t* cnt;
-    const uint32_t* order;
+    const uint32_t* cnt_r;
     uint32_t* off;
+    const int64_t* d_m;
     int64_t* d_p;        // true pair count
     int64_t* d_pc;       // pair count clamped to capacity
     int64_t cap;
-    __device__ uint64_t load(int64_t r) const { return cnt[order[r]]; }
+    __device__ uint64_t load(int64_t r) const { return cnt_r[r]; }
     __device__ void store(int64_t r, uint64_t ex, uint64_t) const {
         off[r] = ex < (uint64_t)cap ? (uint32_t)ex : (uint32_t)cap;
     }
     __device__ void total(uint64_t t) const {
+        const int64_t pc = t < (uint64_t)cap ? (int64_t)t : cap;
         *d_p = (int64_t)t;
-        *d_pc = t < (uint64_t)cap ? (int64_t)t : cap;
+        *d_pc = pc;
+        off[*d_m] = (uint32_t)pc;
     }
 };
 
-// Emission in depth-rank order: rank r writes (tile, r) for every tile of its
-// rectangle, row-major, and its render record.  Because ranks are ordered by
-// (depth bits, Gaussian index), a stable sort of this stream by tile alone is
-// exactly np.argsort(keys, kind="stable") of the reference (tiling.py:159-164).
-template <typename TileT>
-__global__ void k_emit(const uint32_t* __restrict__ order, const uint32_t* __restrict__ off,
-                       const int64_t* __restrict__ d_m, const adr_projection proj, int32_t tiles_x,
-                       int32_t tiles_y, int64_t cap, TileT* __restrict__ tiles, uint32_t* __restrict__ ranks,
-                       Record* __restrict__ rec) {
+// Per-rank preparation (coalesced by rank): rinfo[r] = (x-range, y-range,
+// Gaussian index, depth bits) gathered from the packed per-Gaussian word
+// stage 1 wrote, plus the pair count of the rank.
+__global__ void k_rank_prepare(const uint32_t* __restrict__ order, const int64_t* __restrict__ d_m,
+                               const uint4* __restrict__ gpack, uint4* __restrict__ rinfo,
+                               uint32_t* __restrict__ cnt_r) {
     const int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (r >= *d_m) return;
     const uint32_t g = order[r];
-    const float2 m = reinterpret_cast<const float2*>(proj.d_mean2d)[g];
-    const Rect rc = tile_rect(m.x, m.y, proj.d_ext_x[g], proj.d_ext_y[g], true, tiles_x, tiles_y);
-    int64_t o = off[r];
-    for (int32_t ty = rc.y0; ty < rc.y1; ++ty)
-        for (int32_t tx = rc.x0; tx < rc.x1; ++tx) {
-            if (o < cap) {
-                tiles[o] = (TileT)(ty * tiles_x + tx);
-                ranks[o] = (uint32_t)r;
-            }
-            ++o;
-        }
-    Record R;
-    R.a = make_float4(m.x, m.y, proj.d_conic[3 * g], proj.d_conic[3 * g + 1]);
-    R.b = make_float4(proj.d_conic[3 * g + 2], proj.d_opacity[g], proj.d_color[3 * g], proj.d_color[3 * g + 1]);
-    R.c = make_float4(proj.d_color[3 * g + 2], 0.f, 0.f, 0.f);
-    rec[r] = R;
+    uint4 inf = gpack[g];
+    inf.z = g;
+    rinfo[r] = inf;
+    cnt_r[r] = ((inf.x >> 16) - (inf.x & 0xffffu)) * ((inf.y >> 16) - (inf.y & 0xffffu));
 }
 
+// ---- rank-ordered pair stream ---------------------------------------------
+// Rank r owns stream positions [off[r], off[r+1]), row-major over its tile
+// rectangle.  A stable sort of this stream by tile is exactly the reference's
+// np.argsort(keys, kind="stable") (tiling.py:159-164) because ranks are
+// ordered by (depth bits, Gaussian index).
+
+constexpr int kEmitWarps = 8;
+constexpr int kEmitStage = 1024;   // staged positions per warp and piece
+
+// Emission of the rank-ordered stream as (tile id, Gaussian index).  A warp
+// owns 32 consecutive ranks, i.e. the contiguous stream range
+// [off[r0], off[r0+32]); each lane expands its own rectangle row-major into a
+// per-warp shared-memory staging buffer, and the warp then copies the staged
+// piece out with coalesced stores.
+template <typename TileT>
+__global__ void __launch_bounds__(kEmitWarps * 32)
+k_emit_stage(const uint4* __restrict__ rinfo, const uint32_t* __restrict__ off, const int64_t* __restrict__ d_m,
+             const int64_t* __restrict__ d_pc, int32_t tiles_x, TileT* __restrict__ tiles, uint32_t* __restrict__ gs) {
+    extern __shared__ __align__(16) unsigned char emit_smem[];
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    TileT* st_t = reinterpret_cast<TileT*>(emit_smem) + warp * kEmitStage;
+    uint32_t* st_g = reinterpret_cast<uint32_t*>(emit_smem + sizeof(TileT) * kEmitWarps * kEmitStage) + warp * kEmitStage;
+    const uint32_t m = (uint32_t)*d_m;
+    const uint32_t pc = (uint32_t)*d_pc;
+    const uint32_t r0 = (blockIdx.x * kEmitWarps + warp) * 32u;
+    if (r0 >= m) return;
+    const uint32_t r = r0 + lane;
+    const bool valid = r < m;
+    const uint4 inf = valid ? rinfo[r] : make_uint4(0, 0, 0, 0);
+    const uint32_t x0 = inf.x & 0xffffu, x1 = inf.x >> 16, y0 = inf.y & 0xffffu, y1 = inf.y >> 16;
+    const uint32_t wdt = x1 - x0;
+    const uint32_t o = valid ? off[r] : pc;
+    const uint32_t c = valid ? wdt * (y1 - y0) : 0u;
+    const uint32_t wstart = __shfl_sync(kFull, o, 0);
+    uint32_t wend = r0 + 32 < m ? off[r0 + 32] : pc;
+    wend = wend < pc ? wend : pc;
+    const uint32_t oe = o + c;
+    for (uint32_t ps = wstart; ps < wend; ps += kEmitStage) {
+        const uint32_t pe = ps + kEmitStage < wend ? ps + kEmitStage : wend;
+        const uint32_t a = o > ps ? o : ps;
+        const uint32_t b = oe < pe ? oe : pe;
+        if (a < b) {
+            uint32_t j = a - o;
+            uint32_t ty = y0 + j / wdt;
+            uint32_t tx = x0 + (j - (ty - y0) * wdt);
+            for (uint32_t q = a - ps; q < b - ps; ++q) {
+                st_t[q] = (TileT)(ty * (uint32_t)tiles_x + tx);
+                st_g[q] = inf.z;
+                if (++tx == x1) {
+                    tx = x0;
+                    ++ty;
+                }
+            }
+        }
+        __syncwarp();
+        for (uint32_t q = lane; q < pe - ps; q += 32) {
+            tiles[ps + q] = st_t[q];
+            gs[ps + q] = st_g[q];
+        }
+        __syncwarp();
+    }
+}
+
+// ranges[t] = (lower_bound(t), lower_bound(t+1)) over sorted tile ids; each
+// thread owns 8 consecutive positions (one 16-byte load for u16 ids) and
+// writes the boundaries that fall on them; position p (the end) is owned by
+// the thread whose range contains it.
 template <typename TileT>
 __global__ void k_ranges_tiles(const TileT* __restrict__ tiles, const int64_t* __restrict__ d_p, int64_t n_tiles,
                                int64_t* __restrict__ ranges) {
     const int64_t p = *d_p;
-    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i <= p; i += (int64_t)gridDim.x * blockDim.x) {
-        const int64_t t_prev = i == 0 ? -1 : (int64_t)tiles[i - 1];
-        const int64_t t_cur = i < p ? (int64_t)tiles[i] : n_tiles;
-        write_bounds<TileT>(i, t_prev, t_cur, n_tiles, ranges);
+    const int64_t i0 = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) * 8;
+    if (i0 > p) return;
+    TileT v[9];
+    v[0] = i0 == 0 ? TileT(0) : tiles[i0 - 1];
+    if (sizeof(TileT) == 2 && i0 + 8 <= p) {
+        const uint4 q = *reinterpret_cast<const uint4*>(tiles + i0);
+#pragma unroll
+        for (int k = 0; k < 8; ++k) v[k + 1] = reinterpret_cast<const TileT*>(&q)[k];
+    } else {
+#pragma unroll
+        for (int k = 0; k < 8; ++k) v[k + 1] = i0 + k < p ? tiles[i0 + k] : TileT(0);
     }
-}
-
-template <typename TileT>
-__global__ void k_export(const TileT* __restrict__ tiles, const uint32_t* __restrict__ ranks,
-                         const uint32_t* __restrict__ order, const float* __restrict__ depth,
-                         const int64_t* __restrict__ d_p, uint64_t* __restrict__ keys, int32_t* __restrict__ gidx) {
-    const int64_t p = *d_p;
-    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < p; i += (int64_t)gridDim.x * blockDim.x) {
-        const uint32_t g = order[ranks[i]];
-        if (keys) keys[i] = ((uint64_t)tiles[i] << 32) | __float_as_uint(depth[g]);
-        if (gidx) gidx[i] = (int32_t)g;
+#pragma unroll
+    for (int k = 0; k < 8; ++k) {
+        const int64_t i = i0 + k;
+        if (i > p) break;
+        const int64_t prev = i == 0 ? -1 : (int64_t)v[k];
+        const int64_t cur = i < p ? (int64_t)v[k + 1] : n_tiles;
+        if (cur != prev) write_bounds<TileT>(i, prev, cur, n_tiles, ranges);
     }
-}
-
-int grid_stride_blocks(int64_t work, int block) {
-    int64_t b = ceil_div(work > 0 ? work : 1, block);
-    const int64_t cap = 148 * 16;
-    return (int)(b < cap ? b : cap);
 }
 
 }  // namespace
 
 size_t frame_binning_scratch(int64_t n, int64_t cap, int64_t n_tiles) {
+    const int64_t nlb = ceil_div(n > 0 ? n : 1, kLbTile);
     const bool wide = n_tiles > 65536;
     const size_t tile_sz = wide ? 4 : 2;
-    const int64_t nlb = ceil_div(n > 0 ? n : 1, kLbTile);
     size_t s = 0;
-    s += align_up(4 * (size_t)n) * 6;                       // cnt, sel_key, sel_idx, skey, order, off
-    s += align_up(sizeof(Record) * (size_t)n);              // records
+    s += align_up(4 * (size_t)n) * 4 + align_up(4 * (size_t)(n + 1));  // sel_key, sel_idx, skey, cnt_r, off
+    s += align_up(16 * (size_t)n);                                     // rinfo
     s += radix_scratch_bytes<uint32_t, uint32_t>(n);
-    s += 2 * (align_up(tile_sz * (size_t)cap) + align_up(4 * (size_t)cap));  // tiles, ranks (+sorted)
-    s += wide ? radix_scratch_bytes<uint32_t, uint32_t>(cap) : radix_scratch_bytes<uint16_t, uint32_t>(cap);
     s += 2 * lookback_bytes(nlb);
-    return s + 4096;
+    s += 2 * align_up(tile_sz * (size_t)cap) + align_up(4 * (size_t)cap);  // tiles, sorted tiles, gs
+    s += wide ? radix_scratch_bytes<uint32_t, uint32_t>(cap) : radix_scratch_bytes<uint16_t, uint32_t>(cap);
+    return s + 8192;
 }
 
 template <typename TileT>
 static int32_t frame_binning_t(const FrameBinning& fb, cudaStream_t st) {
     Carver c(fb.scratch, fb.scratch_bytes);
     const int64_t n = fb.n, cap = fb.cap;
-    uint32_t* cnt = fb.cnt;
     uint32_t* sel_key = c.take<uint32_t>(n);
     uint32_t* sel_idx = c.take<uint32_t>(n);
     uint32_t* skey = c.take<uint32_t>(n);
-    uint32_t* order = fb.order;
-    uint32_t* off = c.take<uint32_t>(n);
-    Record* rec = fb.rec;
+    uint32_t* cnt_r = c.take<uint32_t>(n);
+    uint32_t* off = c.take<uint32_t>(n + 1);
+    uint4* rinfo = c.take<uint4>(n);
     void* rs1 = c.take<char>((int64_t)radix_scratch_bytes<uint32_t, uint32_t>(n));
-    TileT* tiles = c.take<TileT>(cap);
-    uint32_t* ranks = c.take<uint32_t>(cap);
-    TileT* stiles = c.take<TileT>(cap);
-    uint32_t* sranks = fb.sorted_ranks;
-    void* rs2 = c.take<char>((int64_t)radix_scratch_bytes<TileT, uint32_t>(cap));
     const int64_t nlb = ceil_div(n, kLbTile);
     uint64_t* st1 = c.take<uint64_t>(nlb + 1);
     uint64_t* st2 = c.take<uint64_t>(nlb + 1);
+    TileT* tiles = c.take<TileT>(cap);
+    TileT* stiles = c.take<TileT>(cap);
+    uint32_t* gs = c.take<uint32_t>(cap);
+    void* rs2 = c.take<char>((int64_t)radix_scratch_bytes<TileT, uint32_t>(cap));
     if (!c.ok()) return fail(ADR_ERR_VALUE, "render_frame: scratch too small");
     int64_t* ctr = fb.counters;  // [0]=P, [1]=culled, [2]=M, [3]=P clamped
+    uint32_t* order = fb.order;
 
     // (a) compaction of Gaussians with pairs, keyed by depth bits
     ADR_CUDA_TRY(cudaMemsetAsync(st1, 0, sizeof(uint64_t) * (nlb + 1), st));
-    SelectOp sel{cnt, fb.proj.d_depth, sel_key, sel_idx, ctr + 2};
+    SelectOp sel{fb.cnt, fb.proj.d_depth, sel_key, sel_idx, ctr + 2};
     k_scan_lookback<SelectOp><<<nlb, kLbBlock, 0, st>>>(sel, nullptr, n, st1, reinterpret_cast<unsigned long long*>(st1 + nlb));
     ADR_LAUNCH_CHECK();
     // (b) stable depth sort of the M survivors -> order[rank] (ties by index)
     int32_t rc = radix_sort<uint32_t, uint32_t>(sel_key, sel_idx, skey, order, ctr + 2, n, 31, rs1,
                                                 radix_scratch_bytes<uint32_t, uint32_t>(n), st);
     if (rc) return rc;
-    // (c) pair offsets in rank order, P
+    // (c) per-rank rectangles, then pair offsets in rank order and P
+    k_rank_prepare<<<ceil_div(n, 256), 256, 0, st>>>(order, ctr + 2, fb.gpack, rinfo, cnt_r);
+    ADR_LAUNCH_CHECK();
     ADR_CUDA_TRY(cudaMemsetAsync(st2, 0, sizeof(uint64_t) * (nlb + 1), st));
-    OffsetsOp oo{cnt, order, off, ctr + 0, ctr + 3, cap};
+    OffsetsOp oo{cnt_r, off, ctr + 2, ctr + 0, ctr + 3, cap};
     k_scan_lookback<OffsetsOp><<<nlb, kLbBlock, 0, st>>>(oo, ctr + 2, n, st2, reinterpret_cast<unsigned long long*>(st2 + nlb));
     ADR_LAUNCH_CHECK();
     if (fb.ev_after_scan) ADR_CUDA_TRY(cudaEventRecord(fb.ev_after_scan, st));
-    // (d) emission + records
-    k_emit<TileT><<<ceil_div(n, 128), 128, 0, st>>>(order, off, ctr + 2, fb.proj, fb.tiles_x, fb.tiles_y, cap, tiles,
-                                                    ranks, rec);
-    ADR_LAUNCH_CHECK();
-    if (fb.ev_after_dup) ADR_CUDA_TRY(cudaEventRecord(fb.ev_after_dup, st));
-    // (e) stable sort by tile id
+    // (d) emission of the stream as (tile, Gaussian)
     int tbits = 0;
     while ((int64_t(1) << tbits) < fb.n_tiles) ++tbits;
-    rc = radix_sort<TileT, uint32_t>(tiles, ranks, stiles, sranks, ctr + 3, cap, tbits, rs2,
-                                     radix_scratch_bytes<TileT, uint32_t>(cap), st);
+    if (tbits == 0) tbits = 1;
+    {
+        const size_t esm = (sizeof(TileT) + sizeof(uint32_t)) * kEmitWarps * kEmitStage;
+        ADR_CUDA_TRY(cudaFuncSetAttribute(k_emit_stage<TileT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)esm));
+        k_emit_stage<TileT><<<ceil_div(n, kEmitWarps * 32), kEmitWarps * 32, esm, st>>>(rinfo, off, ctr + 2, ctr + 3,
+                                                                                        fb.tiles_x, tiles, gs);
+        ADR_LAUNCH_CHECK();
+    }
+    if (fb.ev_after_dup) ADR_CUDA_TRY(cudaEventRecord(fb.ev_after_dup, st));
+    // (e) stable radix sort by tile id; the last pass writes the sorted
+    //     Gaussian indices (the render's record index and the gidx export)
+    //     and the reference-layout keys (tile << 32 | depth bits)
+    rc = radix_sort<TileT, uint32_t>(tiles, gs, stiles, reinterpret_cast<uint32_t*>(fb.gidx), ctr + 3, cap, tbits,
+                                     rs2, radix_scratch_bytes<TileT, uint32_t>(cap), st, fb.proj.d_depth, fb.keys);
     if (rc) return rc;
     if (fb.ev_after_sort) ADR_CUDA_TRY(cudaEventRecord(fb.ev_after_sort, st));
     // (f) tile ranges
-    k_ranges_tiles<TileT><<<grid_stride_blocks(cap + 1, 256), 256, 0, st>>>(stiles, ctr + 3, fb.n_tiles, fb.ranges);
+    k_ranges_tiles<TileT><<<ceil_div(ceil_div(cap + 1, 8), 256), 256, 0, st>>>(stiles, ctr + 3, fb.n_tiles, fb.ranges);
     ADR_LAUNCH_CHECK();
-    // (g) export of the reference-layout sorted keys / Gaussian indices
-    if (fb.keys || fb.gidx) {
-        k_export<TileT><<<grid_stride_blocks(cap, 256), 256, 0, st>>>(stiles, sranks, order, fb.proj.d_depth, ctr + 3,
-                                                                     fb.keys, fb.gidx);
-        ADR_LAUNCH_CHECK();
-    }
     if (fb.ev_after_ranges) ADR_CUDA_TRY(cudaEventRecord(fb.ev_after_ranges, st));
     return ADR_OK;
 }
@@ -421,6 +475,8 @@ int32_t frame_binning(const FrameBinning& fb, cudaStream_t st) {
     if (fb.n <= 0) return ADR_OK;
     if (fb.n >= (int64_t(1) << 31)) return fail(ADR_ERR_CAPACITY, "more than 2^31 Gaussians");
     if (fb.cap >= (int64_t(1) << 31)) return fail(ADR_ERR_CAPACITY, "pair capacity must be < 2^31");
+    if (fb.tiles_x >= 65536 || fb.tiles_y >= 65536) return fail(ADR_ERR_CAPACITY, "tile grid side >= 65536");
+    if (!fb.gidx) return fail(ADR_ERR_VALUE, "render_frame needs the sorted index buffer");
     return fb.n_tiles > 65536 ? frame_binning_t<uint32_t>(fb, st) : frame_binning_t<uint16_t>(fb, st);
 }
 

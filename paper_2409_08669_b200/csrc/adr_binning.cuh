@@ -19,7 +19,8 @@ int32_t stage_ranges(const uint64_t* keys, int64_t p, int64_t n_tiles, int64_t* 
                      cudaStream_t st);
 
 // Fused-frame binning: compaction → depth-rank sort of Gaussians → rank-ordered
-// pair emission → stable tile sort → ranges (→ optional reference-layout export).
+// pair emission → stable onesweep tile sort (with the reference-layout export)
+// → tile ranges.
 struct FrameBinning {
     adr_projection proj;
     int64_t n = 0;
@@ -27,12 +28,11 @@ struct FrameBinning {
     int64_t n_tiles = 0;
     int32_t tiles_x = 0, tiles_y = 0;
     uint32_t* cnt = nullptr;    // per-Gaussian touched counts (from stage 1)
-    uint32_t* order = nullptr;  // out: order[rank] = Gaussian index
-    Record* rec = nullptr;      // out: records by rank
-    uint32_t* sorted_ranks = nullptr;  // out: per sorted pair, rank
+    const uint4* gpack = nullptr;  // per-Gaussian packed rect + depth bits (stage 1)
+    uint32_t* order = nullptr;  // scratch: order[rank] = Gaussian index
     int64_t* ranges = nullptr;  // out: (n_tiles, 2)
-    uint64_t* keys = nullptr;   // optional export
-    int32_t* gidx = nullptr;    // optional export
+    uint64_t* keys = nullptr;   // optional out: sorted keys (tile << 32 | depth bits)
+    int32_t* gidx = nullptr;    // out: sorted Gaussian indices (render record index)
     int64_t* counters = nullptr;
     void* scratch = nullptr;
     size_t scratch_bytes = 0;

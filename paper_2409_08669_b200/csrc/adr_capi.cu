@@ -32,7 +32,7 @@ struct FrameLayout {
     uint32_t* cnt;
     uint32_t* order;
     Record* rec;
-    uint32_t* sorted_ranks;
+    uint4* gpack;
     void* binning;
     size_t binning_bytes;
 };
@@ -43,7 +43,7 @@ size_t frame_bytes(int64_t n, int64_t n_tiles, int64_t cap, FrameLayout* out, vo
     l.cnt = c.take<uint32_t>(n);
     l.order = c.take<uint32_t>(n);
     l.rec = c.take<Record>(n);
-    l.sorted_ranks = c.take<uint32_t>(cap);
+    l.gpack = c.take<uint4>(n);
     l.binning_bytes = frame_binning_scratch(n, cap, n_tiles);
     l.binning = c.take<char>((int64_t)l.binning_bytes);
     if (out) *out = l;
@@ -148,6 +148,8 @@ int32_t adr_render_frame(const adr_scene* scene, const adr_camera* cam, int32_t 
     if (ev[0]) ADR_CUDA_TRY(cudaEventRecord(ev[0], st));
     FusedPre fp;
     fp.cnt = L.cnt;
+    fp.rec = L.rec;
+    fp.gpack = L.gpack;
     fp.culled = reinterpret_cast<unsigned long long*>(buf->d_counters + 1);
     fp.tiles_x = tx;
     fp.tiles_y = ty;
@@ -165,8 +167,7 @@ int32_t adr_render_frame(const adr_scene* scene, const adr_camera* cam, int32_t 
         fb.tiles_y = ty;
         fb.cnt = L.cnt;
         fb.order = L.order;
-        fb.rec = L.rec;
-        fb.sorted_ranks = L.sorted_ranks;
+        fb.gpack = L.gpack;
         fb.ranges = buf->d_ranges;
         fb.keys = buf->d_keys;
         fb.gidx = buf->d_gidx;
@@ -189,7 +190,7 @@ int32_t adr_render_frame(const adr_scene* scene, const adr_camera* cam, int32_t 
     if (rc) return rc;
     RenderArgs ra;
     ra.rec = L.rec;
-    ra.idx = L.sorted_ranks;
+    ra.idx = reinterpret_cast<const uint32_t*>(buf->d_gidx);
     ra.ranges = buf->d_ranges;
     ra.width = cam->width;
     ra.height = cam->height;

@@ -5,9 +5,19 @@
 
 namespace adr {
 
+// Render-side per-Gaussian record (indexed by Gaussian), 48 bytes.
+//   a = (mx, my, conic_a, conic_b)
+//   b = (conic_c, opacity, r, g)
+//   c = (b, unused, unused, unused)
+struct __align__(16) Record {
+    float4 a, b, c;
+};
+
 // Extra per-Gaussian outputs the fused frame needs from stage 1.
 struct FusedPre {
     uint32_t* cnt = nullptr;                  // touched-tile count (0 when culled)
+    Record* rec = nullptr;                    // render record (valid rows)
+    uint4* gpack = nullptr;                   // (x0 | x1 << 16, y0 | y1 << 16, 0, depth bits)
     unsigned long long* culled = nullptr;     // += number of !valid rows
     int32_t tiles_x = 0, tiles_y = 0;
 };
@@ -15,14 +25,6 @@ struct FusedPre {
 int32_t launch_preprocess(const adr_scene& scene, const adr_camera& cam, int32_t mode,
                           double alpha_low, double dilation, const adr_projection& out,
                           const FusedPre* fused, cudaStream_t st);
-
-// Render-side per-Gaussian record (rank- or gidx-indexed), 48 bytes.
-//   a = (mx, my, conic_a, conic_b)
-//   b = (conic_c, opacity, r, g)
-//   c = (b, unused, unused, unused)
-struct __align__(16) Record {
-    float4 a, b, c;
-};
 
 struct RenderArgs {
     const Record* rec;        // records

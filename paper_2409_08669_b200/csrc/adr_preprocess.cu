@@ -169,18 +169,25 @@ k_preprocess(const T* __restrict__ centers, const T* __restrict__ scales,
                 col[ch] = sh_channel<DEG>(cf, d0, d1, d2);
             }
             const float2 m2 = make_float2(__double2float_rn(mx), __double2float_rn(my));
+            const float ca = __double2float_rn(__ddiv_rn(syy, det));
+            const float cb = __double2float_rn(__ddiv_rn(-sxy, det));
+            const float cc = __double2float_rn(__ddiv_rn(sxx, det));
+            const float dz = __double2float_rn(depth);
+            const float op = __double2float_rn(sigma);
+            const float c0f = __double2float_rn(col[0]), c1f = __double2float_rn(col[1]),
+                        c2f = __double2float_rn(col[2]);
             reinterpret_cast<float2*>(out.d_mean2d)[i] = m2;
             out.d_cov2d[3 * i] = __double2float_rn(sxx);
             out.d_cov2d[3 * i + 1] = __double2float_rn(syy);
             out.d_cov2d[3 * i + 2] = __double2float_rn(sxy);
-            out.d_conic[3 * i] = __double2float_rn(__ddiv_rn(syy, det));
-            out.d_conic[3 * i + 1] = __double2float_rn(__ddiv_rn(-sxy, det));
-            out.d_conic[3 * i + 2] = __double2float_rn(__ddiv_rn(sxx, det));
-            out.d_depth[i] = __double2float_rn(depth);
-            out.d_color[3 * i] = __double2float_rn(col[0]);
-            out.d_color[3 * i + 1] = __double2float_rn(col[1]);
-            out.d_color[3 * i + 2] = __double2float_rn(col[2]);
-            out.d_opacity[i] = __double2float_rn(sigma);
+            out.d_conic[3 * i] = ca;
+            out.d_conic[3 * i + 1] = cb;
+            out.d_conic[3 * i + 2] = cc;
+            out.d_depth[i] = dz;
+            out.d_color[3 * i] = c0f;
+            out.d_color[3 * i + 1] = c1f;
+            out.d_color[3 * i + 2] = c2f;
+            out.d_opacity[i] = op;
             out.d_lambda_max[i] = __double2float_rn(lam_max);
             out.d_ext_x[i] = (int32_t)ex;
             out.d_ext_y[i] = (int32_t)ey;
@@ -188,6 +195,13 @@ k_preprocess(const T* __restrict__ centers, const T* __restrict__ scales,
                 const Rect r = tile_rect(m2.x, m2.y, (int32_t)ex, (int32_t)ey, true, fused.tiles_x, fused.tiles_y);
                 const int64_t c = r.count();
                 fused.cnt[i] = (uint32_t)(c < 0xffffffffll ? c : 0xffffffffll);
+                Record R;
+                R.a = make_float4(m2.x, m2.y, ca, cb);
+                R.b = make_float4(cc, op, c0f, c1f);
+                R.c = make_float4(c2f, 0.f, 0.f, 0.f);
+                fused.rec[i] = R;
+                fused.gpack[i] = make_uint4((uint32_t)r.x0 | ((uint32_t)r.x1 << 16),
+                                            (uint32_t)r.y0 | ((uint32_t)r.y1 << 16), 0u, __float_as_uint(dz));
             }
         } else {
             reinterpret_cast<float2*>(out.d_mean2d)[i] = make_float2(0.f, 0.f);

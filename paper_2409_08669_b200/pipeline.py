@@ -136,17 +136,26 @@ class Rasterizer:
         dev = self.device
         if self.export_pairs:
             self.keys = torch.empty(cap, dtype=torch.uint64, device=dev)
-            self.gidx = torch.empty(cap, dtype=torch.int32, device=dev)
+        # sorted Gaussian indices: the render's record index, always produced
+        self.gidx = torch.empty(cap, dtype=torch.int32, device=dev)
         nbytes = _lib.lib().adr_frame_scratch_bytes(self.n, self.width, self.height, cap)
         self.scratch = torch.empty(nbytes, dtype=torch.uint8, device=dev)
         self.cap = cap
+
+    def fit_capacity(self, pairs: int, slack: float = 1.02) -> None:
+        """Size the pair buffers to `pairs` (+slack): grids of the pair-parallel
+        kernels scale with the capacity, so a tight capacity is faster."""
+        cap = int(pairs * slack) + 1024
+        if cap != self.cap:
+            self.cap = 0
+            self._ensure_capacity(cap)
 
     def _buffers(self, timed: bool) -> _lib.FrameBuffers_t:
         b = _lib.FrameBuffers_t()
         b.proj = self.proj.struct()
         b.d_pixels, b.d_load = _lib.ptr(self.pixels), _lib.ptr(self.load)
         b.d_keys = _lib.ptr(self.keys) if self.export_pairs else None
-        b.d_gidx = _lib.ptr(self.gidx) if self.export_pairs else None
+        b.d_gidx = _lib.ptr(self.gidx)
         b.d_ranges, b.d_counters = _lib.ptr(self.ranges), _lib.ptr(self.counters)
         b.d_stats, b.d_hist, b.hist_bins = _lib.ptr(self.stats), None, 0
         b.d_scratch, b.scratch_bytes = _lib.ptr(self.scratch), self.scratch.numel()
@@ -218,11 +227,8 @@ class Rasterizer:
         mx = mx - (1 << 32) if mx >= (1 << 31) else mx
         npx = self.width * self.height
         load_stats = LoadStats.from_moments(npx, int(s[0]), int(s[1]), mn, mx)
-        if self.export_pairs:
-            pairs = TilePairList(keys=self.keys[:p], gaussian_indices=self.gidx[:p],
-                                 tile_ranges=self.ranges)
-        else:
-            pairs = TilePairList(keys=self.keys, gaussian_indices=self.gidx, tile_ranges=self.ranges)
+        keys = self.keys[:p] if self.export_pairs else None
+        pairs = TilePairList(keys=keys, gaussian_indices=self.gidx[:p], tile_ranges=self.ranges)
         return PipelineResult(image=Image(self.width, self.height, self.pixels),
                               load_map=LoadMap(self.width, self.height, self.load), stats=stats,
                               projection=self.proj, pairs=pairs, load_stats=load_stats)

@@ -153,6 +153,26 @@ def test_random_scenes_bitexact_vs_oracle(oracle, seed, count, w, h, deg, mode):
     assert np.array_equal(_np(res.load_map.counts), ref["load"])
 
 
+def test_large_tile_grid_fallback_path_vs_oracle(oracle):
+    """> 16384 tiles takes the emission + radix-sort binning path."""
+    import torch
+
+    import paper_2409_08669_b200 as ab
+
+    a = ab.synthetic_arrays(17, 4000, mixed_spec(), sh_degree=0, float32=True)
+    cam = ab.Camera.from_lookat((0, 0, -3), (0, 0, 0), width=2200, height=2000)
+    assert ab.TileGrid(2200, 2000).n_tiles > 16384
+    res = ab.run_pipeline(ab.DeviceScene.from_arrays(a, 0, "cuda", torch.float32), cam)
+    ref = oracle.run_pipeline(dict(centers=a.centers, scales=a.scales, rotations=a.rotations,
+                                   opacities=a.opacities, sh=a.sh, sh_degree=0), cam, "aabb")
+    p = res.pairs.to_numpy()
+    assert np.array_equal(p["keys"], ref["keys"])
+    assert np.array_equal(p["gaussian_indices"], ref["gidx"])
+    assert np.array_equal(p["tile_ranges"], ref["ranges"])
+    _assert_image(_np(res.image.pixels), ref["pixels"])
+    assert np.array_equal(_np(res.load_map.counts), ref["load"])
+
+
 def test_modes_lossless_and_pairs_monotone():
     """Reference acceptance criterion 1 (+ monotone pairs), size-independent."""
     import torch
