@@ -243,34 +243,20 @@ k_scan_lookback(Op op, const int64_t* d_n, int64_t n_static, uint64_t* status, u
     if (bid == (int64_t)gridDim.x - 1 && threadIdx.x == kLbBlock - 1) op.total(run);
 }
 
-// Compaction of the Gaussians that touch >= 1 tile, in index order, keyed by
-// their float32 depth bits (positive: depth > near_plane > 0).
-struct SelectOp {
-    const uint32_t* cnt;
-    const float* depth;
-    uint32_t* sel_key;
-    uint32_t* sel_idx;
-    int64_t* d_m;
-    __device__ uint64_t load(int64_t i) const { return cnt[i] != 0u ? 1ull : 0ull; }
-    __device__ void store(int64_t i, uint64_t ex, uint64_t v) const {
-        if (v) {
-            sel_key[ex] = __float_as_uint(depth[i]);
-            sel_idx[ex] = (uint32_t)i;
-        }
-    }
-    __device__ void total(uint64_t t) const { *d_m = (int64_t)t; }
-};
-
-// Pair offsets in depth-rank order: off[r] = sum_{r' < r} cnt_r[r'], clamped
-// to the pair capacity; off[M] = min(P, cap) closes the table.
-struct OffsetsOp {
-    const uint32_t* cnt_r;
+// Pair offsets in rank order: off[r] = sum_{r' < r} count(r'), where
+// count(r) is the area of rinfo[r]'s tile rectangle; clamped to the pair
+// capacity, and off[M] = min(P, cap) closes the table.
+struct RankOffsetsOp {
+    const uint4* rinfo;
     uint32_t* off;
     const int64_t* d_m;
     int64_t* d_p;        // true pair count
     int64_t* d_pc;       // pair count clamped to capacity
     int64_t cap;
-    __device__ uint64_t load(int64_t r) const { return cnt_r[r]; }
+    __device__ uint64_t load(int64_t r) const {
+        const uint4 inf = rinfo[r];
+        return (uint64_t)((inf.x >> 16) - (inf.x & 0xffffu)) * ((inf.y >> 16) - (inf.y & 0xffffu));
+    }
     __device__ void store(int64_t r, uint64_t ex, uint64_t) const {
         off[r] = ex < (uint64_t)cap ? (uint32_t)ex : (uint32_t)cap;
     }
@@ -281,21 +267,6 @@ struct OffsetsOp {
         off[*d_m] = (uint32_t)pc;
     }
 };
-
-// Per-rank preparation (coalesced by rank): rinfo[r] = (x-range, y-range,
-// Gaussian index, depth bits) gathered from the packed per-Gaussian word
-// stage 1 wrote, plus the pair count of the rank.
-__global__ void k_rank_prepare(const uint32_t* __restrict__ order, const int64_t* __restrict__ d_m,
-                               const uint4* __restrict__ gpack, uint4* __restrict__ rinfo,
-                               uint32_t* __restrict__ cnt_r) {
-    const int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (r >= *d_m) return;
-    const uint32_t g = order[r];
-    uint4 inf = gpack[g];
-    inf.z = g;
-    rinfo[r] = inf;
-    cnt_r[r] = ((inf.x >> 16) - (inf.x & 0xffffu)) * ((inf.y >> 16) - (inf.y & 0xffffu));
-}
 
 // ---- rank-ordered pair stream ---------------------------------------------
 // Rank r owns stream positions [off[r], off[r+1]), row-major over its tile
@@ -397,10 +368,10 @@ size_t frame_binning_scratch(int64_t n, int64_t cap, int64_t n_tiles) {
     const bool wide = n_tiles > 65536;
     const size_t tile_sz = wide ? 4 : 2;
     size_t s = 0;
-    s += align_up(4 * (size_t)n) * 4 + align_up(4 * (size_t)(n + 1));  // sel_key, sel_idx, skey, cnt_r, off
+    s += align_up(4 * (size_t)n) + align_up(4 * (size_t)(n + 1));      // skey, off
     s += align_up(16 * (size_t)n);                                     // rinfo
     s += radix_scratch_bytes<uint32_t, uint32_t>(n);
-    s += 2 * lookback_bytes(nlb);
+    s += lookback_bytes(nlb);
     s += 2 * align_up(tile_sz * (size_t)cap) + align_up(4 * (size_t)cap);  // tiles, sorted tiles, gs
     s += wide ? radix_scratch_bytes<uint32_t, uint32_t>(cap) : radix_scratch_bytes<uint16_t, uint32_t>(cap);
     return s + 8192;
@@ -410,15 +381,11 @@ template <typename TileT>
 static int32_t frame_binning_t(const FrameBinning& fb, cudaStream_t st) {
     Carver c(fb.scratch, fb.scratch_bytes);
     const int64_t n = fb.n, cap = fb.cap;
-    uint32_t* sel_key = c.take<uint32_t>(n);
-    uint32_t* sel_idx = c.take<uint32_t>(n);
     uint32_t* skey = c.take<uint32_t>(n);
-    uint32_t* cnt_r = c.take<uint32_t>(n);
     uint32_t* off = c.take<uint32_t>(n + 1);
     uint4* rinfo = c.take<uint4>(n);
     void* rs1 = c.take<char>((int64_t)radix_scratch_bytes<uint32_t, uint32_t>(n));
     const int64_t nlb = ceil_div(n, kLbTile);
-    uint64_t* st1 = c.take<uint64_t>(nlb + 1);
     uint64_t* st2 = c.take<uint64_t>(nlb + 1);
     TileT* tiles = c.take<TileT>(cap);
     TileT* stiles = c.take<TileT>(cap);
@@ -426,23 +393,24 @@ static int32_t frame_binning_t(const FrameBinning& fb, cudaStream_t st) {
     void* rs2 = c.take<char>((int64_t)radix_scratch_bytes<TileT, uint32_t>(cap));
     if (!c.ok()) return fail(ADR_ERR_VALUE, "render_frame: scratch too small");
     int64_t* ctr = fb.counters;  // [0]=P, [1]=culled, [2]=M, [3]=P clamped
-    uint32_t* order = fb.order;
 
-    // (a) compaction of Gaussians with pairs, keyed by depth bits
-    ADR_CUDA_TRY(cudaMemsetAsync(st1, 0, sizeof(uint64_t) * (nlb + 1), st));
-    SelectOp sel{fb.cnt, fb.proj.d_depth, sel_key, sel_idx, ctr + 2};
-    k_scan_lookback<SelectOp><<<nlb, kLbBlock, 0, st>>>(sel, nullptr, n, st1, reinterpret_cast<unsigned long long*>(st1 + nlb));
-    ADR_LAUNCH_CHECK();
-    // (b) stable depth sort of the M survivors -> order[rank] (ties by index)
-    int32_t rc = radix_sort<uint32_t, uint32_t>(sel_key, sel_idx, skey, order, ctr + 2, n, 31, rs1,
-                                                radix_scratch_bytes<uint32_t, uint32_t>(n), st);
+    // (a)+(b) stable depth sort of all N Gaussians by the key stage 1 wrote
+    //     (float32 depth bits, all-ones for Gaussians without pairs) with
+    //     the identity as values: ranks [0, M) are the Gaussians with pairs
+    //     ordered by (depth bits, index); the last pass writes, per rank,
+    //     rinfo = (x-range, y-range, Gaussian index, depth bits)
+    SortExtra dx;
+    dx.mode = 2;
+    dx.gsrc = fb.gpack;
+    dx.gdst = rinfo;
+    int32_t rc = radix_sort<uint32_t, uint32_t>(fb.dkey, nullptr, skey, fb.order, nullptr, n, 32, rs1,
+                                                radix_scratch_bytes<uint32_t, uint32_t>(n), st, dx);
     if (rc) return rc;
-    // (c) per-rank rectangles, then pair offsets in rank order and P
-    k_rank_prepare<<<ceil_div(n, 256), 256, 0, st>>>(order, ctr + 2, fb.gpack, rinfo, cnt_r);
-    ADR_LAUNCH_CHECK();
+    // (c) pair offsets in rank order, and P
     ADR_CUDA_TRY(cudaMemsetAsync(st2, 0, sizeof(uint64_t) * (nlb + 1), st));
-    OffsetsOp oo{cnt_r, off, ctr + 2, ctr + 0, ctr + 3, cap};
-    k_scan_lookback<OffsetsOp><<<nlb, kLbBlock, 0, st>>>(oo, ctr + 2, n, st2, reinterpret_cast<unsigned long long*>(st2 + nlb));
+    RankOffsetsOp oo{rinfo, off, ctr + 2, ctr + 0, ctr + 3, cap};
+    k_scan_lookback<RankOffsetsOp><<<nlb, kLbBlock, 0, st>>>(oo, ctr + 2, n, st2,
+                                                            reinterpret_cast<unsigned long long*>(st2 + nlb));
     ADR_LAUNCH_CHECK();
     if (fb.ev_after_scan) ADR_CUDA_TRY(cudaEventRecord(fb.ev_after_scan, st));
     // (d) emission of the stream as (tile, Gaussian)
@@ -460,8 +428,12 @@ static int32_t frame_binning_t(const FrameBinning& fb, cudaStream_t st) {
     // (e) stable radix sort by tile id; the last pass writes the sorted
     //     Gaussian indices (the render's record index and the gidx export)
     //     and the reference-layout keys (tile << 32 | depth bits)
+    SortExtra tx;
+    tx.mode = 1;
+    tx.exp_depth = fb.proj.d_depth;
+    tx.exp_keys = fb.keys;
     rc = radix_sort<TileT, uint32_t>(tiles, gs, stiles, reinterpret_cast<uint32_t*>(fb.gidx), ctr + 3, cap, tbits,
-                                     rs2, radix_scratch_bytes<TileT, uint32_t>(cap), st, fb.proj.d_depth, fb.keys);
+                                     rs2, radix_scratch_bytes<TileT, uint32_t>(cap), st, tx);
     if (rc) return rc;
     if (fb.ev_after_sort) ADR_CUDA_TRY(cudaEventRecord(fb.ev_after_sort, st));
     // (f) tile ranges

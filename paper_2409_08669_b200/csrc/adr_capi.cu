@@ -29,7 +29,7 @@ inline int32_t tiles_of(int32_t v) { return (v + kTile - 1) / kTile; }
 
 // Workspace carve-up of the fused frame (must match adr_frame_scratch_bytes).
 struct FrameLayout {
-    uint32_t* cnt;
+    uint32_t* dkey;
     uint32_t* order;
     Record* rec;
     uint4* gpack;
@@ -40,7 +40,7 @@ struct FrameLayout {
 size_t frame_bytes(int64_t n, int64_t n_tiles, int64_t cap, FrameLayout* out, void* base, size_t cap_bytes) {
     Carver c(base, cap_bytes);
     FrameLayout l;
-    l.cnt = c.take<uint32_t>(n);
+    l.dkey = c.take<uint32_t>(n);
     l.order = c.take<uint32_t>(n);
     l.rec = c.take<Record>(n);
     l.gpack = c.take<uint4>(n);
@@ -147,9 +147,10 @@ int32_t adr_render_frame(const adr_scene* scene, const adr_camera* cam, int32_t 
     ADR_CUDA_TRY(cudaMemsetAsync(buf->d_counters, 0, 8 * sizeof(int64_t), st));
     if (ev[0]) ADR_CUDA_TRY(cudaEventRecord(ev[0], st));
     FusedPre fp;
-    fp.cnt = L.cnt;
     fp.rec = L.rec;
     fp.gpack = L.gpack;
+    fp.dkey = L.dkey;
+    fp.d_m = buf->d_counters + 2;
     fp.culled = reinterpret_cast<unsigned long long*>(buf->d_counters + 1);
     fp.tiles_x = tx;
     fp.tiles_y = ty;
@@ -165,7 +166,7 @@ int32_t adr_render_frame(const adr_scene* scene, const adr_camera* cam, int32_t 
         fb.n_tiles = n_tiles;
         fb.tiles_x = tx;
         fb.tiles_y = ty;
-        fb.cnt = L.cnt;
+        fb.dkey = L.dkey;
         fb.order = L.order;
         fb.gpack = L.gpack;
         fb.ranges = buf->d_ranges;

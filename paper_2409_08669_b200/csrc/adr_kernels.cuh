@@ -15,10 +15,11 @@ struct __align__(16) Record {
 
 // Extra per-Gaussian outputs the fused frame needs from stage 1.
 struct FusedPre {
-    uint32_t* cnt = nullptr;                  // touched-tile count (0 when culled)
     Record* rec = nullptr;                    // render record (valid rows)
     uint4* gpack = nullptr;                   // (x0 | x1 << 16, y0 | y1 << 16, 0, depth bits)
     unsigned long long* culled = nullptr;     // += number of !valid rows
+    uint32_t* dkey = nullptr;                 // depth-sort key (all-ones: no pairs)
+    int64_t* d_m = nullptr;                   // += number of Gaussians with pairs (zeroed)
     int32_t tiles_x = 0, tiles_y = 0;
 };
 

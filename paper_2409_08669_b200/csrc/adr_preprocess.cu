@@ -55,15 +55,61 @@ __device__ __forceinline__ double sh_channel(const double* c, double x, double y
     return np_clip(ADD(r, 0.5), 0.0, 1.0);
 }
 
+constexpr int kPreBlock = 128;
+
+// SH coefficients of the block's Gaussians are staged through shared memory:
+// one coalesced pass over the block's contiguous (128, K, 3) slab, stored with
+// an odd per-Gaussian stride (K*3 + 1 elements) so the per-thread reads of its
+// own coefficients are bank-conflict free.
+template <typename T, int DEG>
+__device__ __forceinline__ void stage_sh(const T* __restrict__ sh, int64_t first, int count, T* stage) {
+    constexpr int K3 = (DEG + 1) * (DEG + 1) * 3;
+    constexpr int S = K3 + 1;
+    const T* src = sh + first * K3;
+    const int total = count * K3;
+    if constexpr (sizeof(T) == 4 && K3 % 4 == 0) {
+        if (count == kPreBlock) {
+            // all K3/4 vector loads of this thread in flight before any store
+            constexpr int kVec = K3 / 4;
+            const float4* s4 = reinterpret_cast<const float4*>(src);
+            float4 v[kVec];
+#pragma unroll
+            for (int u = 0; u < kVec; ++u) v[u] = __ldg(s4 + threadIdx.x + u * kPreBlock);
+#pragma unroll
+            for (int u = 0; u < kVec; ++u) {
+                const int f = 4 * (threadIdx.x + u * kPreBlock), g = f / K3, j = f - g * K3;
+                float* d = reinterpret_cast<float*>(stage) + g * S + j;
+                d[0] = v[u].x;
+                d[1] = v[u].y;
+                d[2] = v[u].z;
+                d[3] = v[u].w;
+            }
+            return;
+        }
+    }
+    for (int f = threadIdx.x; f < total; f += kPreBlock) {
+        const int g = f / K3, j = f - g * K3;
+        stage[g * S + j] = src[f];
+    }
+}
+
 template <typename T, int DEG, bool FUSED>
-__global__ void __launch_bounds__(128)
+__global__ void __launch_bounds__(kPreBlock)
 k_preprocess(const T* __restrict__ centers, const T* __restrict__ scales,
              const T* __restrict__ rotations, const T* __restrict__ opacities,
              const T* __restrict__ sh, int64_t n, adr_camera cam, int32_t mode,
              double alpha_low, double dilation, adr_projection out, FusedPre fused) {
     constexpr int K = (DEG + 1) * (DEG + 1);
-    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    constexpr int S = K * 3 + 1;
+    extern __shared__ __align__(16) unsigned char pre_smem[];
+    T* stage = reinterpret_cast<T*>(pre_smem);
+    const int64_t first = (int64_t)blockIdx.x * kPreBlock;
+    const int64_t i = first + threadIdx.x;
+    stage_sh<T, DEG>(sh, first, (int)(n - first < kPreBlock ? n - first : kPreBlock), stage);
+    __syncthreads();
     bool alive = false;
+    bool selected = false;   // fused: touches >= 1 tile
+    uint32_t dbits = 0;      // fused: float32 depth bits
     if (i < n) {
         const double* R = cam.rot;
         const double c0 = (double)centers[3 * i], c1 = (double)centers[3 * i + 1],
@@ -159,7 +205,7 @@ k_preprocess(const T* __restrict__ centers, const T* __restrict__ scales,
             d0 = __ddiv_rn(d0, dn);
             d1 = __ddiv_rn(d1, dn);
             d2 = __ddiv_rn(d2, dn);
-            const T* shp = sh + i * (K * 3);
+            const T* shp = stage + threadIdx.x * S;
             double col[3];
 #pragma unroll
             for (int ch = 0; ch < 3; ++ch) {
@@ -193,8 +239,8 @@ k_preprocess(const T* __restrict__ centers, const T* __restrict__ scales,
             out.d_ext_y[i] = (int32_t)ey;
             if (FUSED) {
                 const Rect r = tile_rect(m2.x, m2.y, (int32_t)ex, (int32_t)ey, true, fused.tiles_x, fused.tiles_y);
-                const int64_t c = r.count();
-                fused.cnt[i] = (uint32_t)(c < 0xffffffffll ? c : 0xffffffffll);
+                selected = r.count() > 0;
+                dbits = __float_as_uint(dz);
                 Record R;
                 R.a = make_float4(m2.x, m2.y, ca, cb);
                 R.b = make_float4(cc, op, c0f, c1f);
@@ -213,12 +259,20 @@ k_preprocess(const T* __restrict__ centers, const T* __restrict__ scales,
             out.d_lambda_max[i] = 0.f;
             out.d_ext_x[i] = 0;
             out.d_ext_y[i] = 0;
-            if (FUSED) fused.cnt[i] = 0;
         }
     }
     if (FUSED) {
+        // depth-sort key: float32 depth bits for Gaussians touching >= 1
+        // tile (depth > near_plane > 0, so bit 31 is clear), all-ones for the
+        // rest, which a stable sort then leaves behind the M selected ones
+        if (i < n) fused.dkey[i] = selected ? dbits : 0xffffffffu;
+        const int lane = threadIdx.x & 31;
         const uint32_t culled = __ballot_sync(kFull, i < n && !alive);
-        if ((threadIdx.x & 31) == 0 && culled) atomicAdd(fused.culled, (unsigned long long)__popc(culled));
+        const uint32_t sb = __ballot_sync(kFull, selected);
+        if (lane == 0) {
+            if (culled) atomicAdd(fused.culled, (unsigned long long)__popc(culled));
+            if (sb) atomicAdd(reinterpret_cast<unsigned long long*>(fused.d_m), (unsigned long long)__popc(sb));
+        }
     }
 }
 
@@ -230,20 +284,28 @@ k_preprocess(const T* __restrict__ centers, const T* __restrict__ scales,
 template <typename T, bool FUSED>
 int32_t launch_typed(const adr_scene& s, const adr_camera& cam, int32_t mode, double alpha_low,
                      double dilation, const adr_projection& out, const FusedPre& f, cudaStream_t st) {
-    const int block = 128;
-    const int64_t grid = ceil_div(s.n, block);
+    const int64_t grid = ceil_div(s.n, kPreBlock);
     const T* c = static_cast<const T*>(s.d_centers);
     const T* sc = static_cast<const T*>(s.d_scales);
     const T* r = static_cast<const T*>(s.d_rotations);
     const T* o = static_cast<const T*>(s.d_opacities);
     const T* sh = static_cast<const T*>(s.d_sh);
+#define ADR_PRE(DEG)                                                                                          \
+    do {                                                                                                      \
+        const size_t sm = sizeof(T) * kPreBlock * ((DEG + 1) * (DEG + 1) * 3 + 1);                            \
+        ADR_CUDA_TRY(cudaFuncSetAttribute(k_preprocess<T, DEG, FUSED>,                                         \
+                                          cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));             \
+        k_preprocess<T, DEG, FUSED><<<grid, kPreBlock, sm, st>>>(c, sc, r, o, sh, s.n, cam, mode, alpha_low,  \
+                                                                 dilation, out, f);                           \
+    } while (0)
     switch (s.sh_degree) {
-        case 0: k_preprocess<T, 0, FUSED><<<grid, block, 0, st>>>(c, sc, r, o, sh, s.n, cam, mode, alpha_low, dilation, out, f); break;
-        case 1: k_preprocess<T, 1, FUSED><<<grid, block, 0, st>>>(c, sc, r, o, sh, s.n, cam, mode, alpha_low, dilation, out, f); break;
-        case 2: k_preprocess<T, 2, FUSED><<<grid, block, 0, st>>>(c, sc, r, o, sh, s.n, cam, mode, alpha_low, dilation, out, f); break;
-        case 3: k_preprocess<T, 3, FUSED><<<grid, block, 0, st>>>(c, sc, r, o, sh, s.n, cam, mode, alpha_low, dilation, out, f); break;
+        case 0: ADR_PRE(0); break;
+        case 1: ADR_PRE(1); break;
+        case 2: ADR_PRE(2); break;
+        case 3: ADR_PRE(3); break;
         default: return fail(ADR_ERR_VALUE, "sh_degree must be in 0..3");
     }
+#undef ADR_PRE
     ADR_LAUNCH_CHECK();
     return ADR_OK;
 }

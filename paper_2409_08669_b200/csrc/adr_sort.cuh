@@ -1,6 +1,6 @@
 // adr_sort.cuh — stable LSD radix sort (key, value) for sm_100a.
 //
-// Reduce-then-scan per digit pass (<= 7-bit digits):
+// Reduce-then-scan per digit pass (<= 8-bit digits):
 //
 //   upsweep   : block digit histogram with shared-memory atomics ->
 //               digit-major histogram over blocks.
@@ -25,7 +25,7 @@ namespace adr {
 
 constexpr int kSortBlock = 256;
 constexpr int kSortWarps = kSortBlock / 32;
-constexpr int kMaxRadixBits = 7;
+constexpr int kMaxRadixBits = 8;
 
 template <typename K>
 struct SortCfg {
@@ -119,14 +119,23 @@ scan_u32_exclusive(uint32_t* __restrict__ data, int64_t n, uint64_t* status, uns
 }
 
 // Downsweep of one pass (warp-striped: round r, lane l -> item wbase+32r+l,
-// so (round, lane) order is input order).  With EXPORT, also writes
-// exp_keys[g] = key << 32 | float bits of exp_depth[value] (reference keys).
-template <typename K, typename V, int RB, bool EXPORT>
+// so (round, lane) order is input order).  vals_in == nullptr means the
+// identity (value = input index).  Last-pass extras (MODE):
+//   1: exp_keys[g] = key << 32 | float bits of exp_depth[value]  (reference keys)
+//   2: gdst[g] = gsrc[value] with .z = value, and no key/value output
+struct SortExtra {
+    int mode = 0;
+    const float* exp_depth = nullptr;
+    uint64_t* exp_keys = nullptr;
+    const uint4* gsrc = nullptr;
+    uint4* gdst = nullptr;
+};
+
+template <typename K, typename V, int RB, int MODE>
 __global__ void __launch_bounds__(kSortBlock, 3)
 radix_downsweep(const K* __restrict__ keys_in, const V* __restrict__ vals_in, K* __restrict__ keys_out,
                 V* __restrict__ vals_out, const int64_t* d_n, int64_t n_static, int bit,
-                const uint32_t* __restrict__ offsets, const float* __restrict__ exp_depth,
-                uint64_t* __restrict__ exp_keys) {
+                const uint32_t* __restrict__ offsets, SortExtra ex) {
     constexpr int R = 1 << RB;
     constexpr int kIpt = SortCfg<K>::kIpt;
     constexpr int kTile = SortCfg<K>::kTileItems;
@@ -150,7 +159,7 @@ radix_downsweep(const K* __restrict__ keys_in, const V* __restrict__ vals_in, K*
     for (int r = 0; r < kIpt; ++r) {
         const int64_t i = wbase + r * 32 + lane;
         kr[r] = i < n ? keys_in[i] : K(0);
-        vr[r] = i < n ? vals_in[i] : V(0);
+        vr[r] = i < n ? (vals_in ? vals_in[i] : V(i)) : V(0);
     }
     __syncthreads();
     // ranks packed two per register (rank within warp < 32 * kIpt <= 512)
@@ -205,9 +214,16 @@ radix_downsweep(const K* __restrict__ keys_in, const V* __restrict__ vals_in, K*
         const K key = skeys[i];
         const V val = svals[i];
         const int64_t g = goff[digit_of(key, bit, R - 1)] + i;
-        keys_out[g] = key;
-        vals_out[g] = val;
-        if (EXPORT && exp_keys) exp_keys[g] = ((uint64_t)key << 32) | __float_as_uint(exp_depth[val]);
+        if (MODE == 2) {
+            uint4 inf = ex.gsrc[val];
+            inf.z = (uint32_t)val;
+            ex.gdst[g] = inf;
+        } else {
+            keys_out[g] = key;
+            vals_out[g] = val;
+            if (MODE == 1 && ex.exp_keys)
+                ex.exp_keys[g] = ((uint64_t)key << 32) | __float_as_uint(ex.exp_depth[val]);
+        }
     }
 }
 
@@ -230,14 +246,16 @@ inline size_t radix_scratch_bytes(int64_t n_max) {
 inline int pass_count(int end_bit) { return (end_bit + kMaxRadixBits - 1) / kMaxRadixBits; }
 
 // Host driver: sorts n items (live count optionally on device) on bits
-// [0, end_bit).  Output lands in keys_out/vals_out; inputs are untouched.
-// With `exp_depth`, the last pass also writes the reference-layout keys.
+// [0, end_bit).  Output lands in keys_out/vals_out (unless extra.mode == 2);
+// inputs are untouched; vals_in == nullptr sorts the identity permutation.
 template <typename K, typename V>
 int32_t radix_sort(const K* keys_in, const V* vals_in, K* keys_out, V* vals_out, const int64_t* d_n,
                    int64_t n_max, int end_bit, void* scratch, size_t scratch_bytes, cudaStream_t st,
-                   const float* exp_depth = nullptr, uint64_t* exp_keys = nullptr) {
+                   const SortExtra& extra = SortExtra()) {
     if (n_max <= 0) return ADR_OK;
     const int passes = pass_count(end_bit);
+    if (passes == 0 && (!vals_in || extra.mode != 0))
+        return fail(ADR_ERR_VALUE, "radix_sort: identity values / extras need >= 1 pass");
     if (passes == 0) {
         ADR_CUDA_TRY(cudaMemcpyAsync(keys_out, keys_in, sizeof(K) * n_max, cudaMemcpyDeviceToDevice, st));
         ADR_CUDA_TRY(cudaMemcpyAsync(vals_out, vals_in, sizeof(V) * n_max, cudaMemcpyDeviceToDevice, st));
@@ -271,16 +289,22 @@ int32_t radix_sort(const K* keys_in, const V* vals_in, K* keys_out, V* vals_out,
         scan_u32_exclusive<8><<<ceil_div(hl, 256 * 8), 256, 0, st>>>(hist, hl, status, counter);              \
         ADR_LAUNCH_CHECK();                                                                                   \
         const size_t dsm = downsweep_smem<K, V, RB>();                                                        \
-        if (last && exp_depth) {                                                                              \
-            ADR_CUDA_TRY(cudaFuncSetAttribute(radix_downsweep<K, V, RB, true>,                                \
+        const int mode = last ? extra.mode : 0;                                                               \
+        if (mode == 1) {                                                                                      \
+            ADR_CUDA_TRY(cudaFuncSetAttribute(radix_downsweep<K, V, RB, 1>,                                   \
                                               cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dsm));        \
-            radix_downsweep<K, V, RB, true><<<nb, kSortBlock, dsm, st>>>(src_k, src_v, dst_k, dst_v, d_n,     \
-                                                                         n_max, bit, hist, exp_depth, exp_keys); \
+            radix_downsweep<K, V, RB, 1><<<nb, kSortBlock, dsm, st>>>(src_k, src_v, dst_k, dst_v, d_n, n_max,  \
+                                                                      bit, hist, extra);                      \
+        } else if (mode == 2) {                                                                               \
+            ADR_CUDA_TRY(cudaFuncSetAttribute(radix_downsweep<K, V, RB, 2>,                                   \
+                                              cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dsm));        \
+            radix_downsweep<K, V, RB, 2><<<nb, kSortBlock, dsm, st>>>(src_k, src_v, dst_k, dst_v, d_n, n_max,  \
+                                                                      bit, hist, extra);                      \
         } else {                                                                                              \
-            ADR_CUDA_TRY(cudaFuncSetAttribute(radix_downsweep<K, V, RB, false>,                               \
+            ADR_CUDA_TRY(cudaFuncSetAttribute(radix_downsweep<K, V, RB, 0>,                                   \
                                               cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dsm));        \
-            radix_downsweep<K, V, RB, false><<<nb, kSortBlock, dsm, st>>>(src_k, src_v, dst_k, dst_v, d_n,    \
-                                                                          n_max, bit, hist, nullptr, nullptr); \
+            radix_downsweep<K, V, RB, 0><<<nb, kSortBlock, dsm, st>>>(src_k, src_v, dst_k, dst_v, d_n, n_max,  \
+                                                                      bit, hist, extra);                      \
         }                                                                                                     \
         ADR_LAUNCH_CHECK();                                                                                   \
     } while (0)
@@ -291,7 +315,8 @@ int32_t radix_sort(const K* keys_in, const V* vals_in, K* keys_out, V* vals_out,
             case 4: ADR_SORT_PASS(4); break;
             case 5: ADR_SORT_PASS(5); break;
             case 6: ADR_SORT_PASS(6); break;
-            default: ADR_SORT_PASS(7); break;
+            case 7: ADR_SORT_PASS(7); break;
+            default: ADR_SORT_PASS(8); break;
         }
 #undef ADR_SORT_PASS
         bit += bits;
