@@ -154,6 +154,17 @@ int32_t adr_render(const adr_projection* proj, int64_t n, const int64_t* d_gidx,
                    double term_threshold, float* d_pixels, int32_t* d_counts,
                    adr_load_stats* d_stats, int32_t* d_hist, int32_t hist_bins, void* stream);
 
+/* ------------------------------------------------------- numerics checks */
+
+/* The render's float32 exp (restatement of numpy's, sb/render.py:96) on n
+ * device floats, for golden-vector tests. */
+int32_t adr_exp_np_f32(const float* d_x, float* d_y, int64_t n, void* stream);
+
+/* Exhaustive check of the render's exp fast path against the full exp on
+ * every float32 in [-87, 88]: d_result[0] = mismatches, d_result[1] = inputs
+ * checked, d_result[2] = smallest mismatching bit pattern (all-ones if none). */
+int32_t adr_selftest_exp(uint64_t* d_result, void* stream);
+
 /* --------------------------------------------- fused pipeline (run_pipeline)
  * sb/pipeline.py:85-124.  The frame runs as a fixed kernel sequence with no
  * host synchronisation, so it can be captured into a CUDA graph.  Pair

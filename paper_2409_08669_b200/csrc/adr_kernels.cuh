@@ -8,10 +8,56 @@ namespace adr {
 // Render-side per-Gaussian record (indexed by Gaussian), 48 bytes.
 //   a = (mx, my, conic_a, conic_b)
 //   b = (conic_c, opacity, r, g)
-//   c = (b, unused, unused, unused)
+//   c = (b, tau, hx, hy)   -- conservative culling parameters, see cull_params
 struct __align__(16) Record {
     float4 a, b, c;
 };
+
+// Exact-safe culling parameters of one splat for the fp32 blend of
+// sb/render.py:93-97 (alpha = min(sigma * exp_np(power), 0.99), skipped when
+// alpha < alpha_low):
+//   tau      : power < tau  =>  alpha < alpha_low.  exp_np is within 2 ulp of
+//              exp and the product adds one rounding, so
+//              ln(alpha_low / sigma) - 1e-5 (rounded down) is a strict bound.
+//   (hx, hy) : every pixel with |px - mx| > hx or |py - my| > hy has
+//              power < tau *as computed in fp32*: the box of the ellipse
+//              Q(d) <= -2 tau, inflated by s = sqrt((1 + 1e-4) / (1 - eta))
+//              where eta bounds the relative fp32 evaluation error of power
+//              (8 ulp * (max|a|,|c| + |b|/2) / lambda_min), plus 1e-3 px.
+//              Non-positive-definite or ill-conditioned conics get an
+//              infinite box (no culling).
+// A contribution is only skipped when the reference provably skips it, so
+// the image and load map stay bit-identical.
+__device__ inline void cull_params(float a, float b, float c, float op, float alpha_low32, float* tau,
+                                            float* hx, float* hy) {
+    const float kInf = __int_as_float(0x7f800000);
+    if (!(op > 0.0f)) {
+        *tau = kInf;
+        *hx = *hy = 0.0f;
+        return;
+    }
+    const double t = log((double)alpha_low32 / (double)op) - 1e-5;
+    const float t32 = __double2float_rd(t);
+    *tau = t32;
+    *hx = *hy = kInf;
+    const double K = -2.0 * (double)t32;
+    const double da = a, db = b, dc = c;
+    const double det = da * dc - db * db;
+    if (!(det > 0.0) || !(da > 0.0) || !(dc > 0.0)) return;
+    const double half = 0.5 * (da + dc), rad = sqrt(0.25 * (da - dc) * (da - dc) + db * db);
+    const double lmin = half - rad;
+    if (!(lmin > 0.0)) return;
+    const double M = (da > dc ? da : dc) + 0.5 * fabs(db);
+    const double eta = 2.0 * 8.0 * 5.9604644775390625e-08 * M / lmin;
+    if (!(eta < 0.25)) return;
+    if (K <= 0.0) {
+        *hx = *hy = 1.0f;
+        return;
+    }
+    const double s = sqrt((1.0 + 1e-4) / (1.0 - eta));
+    *hx = __double2float_ru(s * sqrt(K * dc / det) + 1e-3);
+    *hy = __double2float_ru(s * sqrt(K * da / det) + 1e-3);
+}
 
 // Extra per-Gaussian outputs the fused frame needs from stage 1.
 struct FusedPre {

@@ -242,9 +242,11 @@ k_preprocess(const T* __restrict__ centers, const T* __restrict__ scales,
                 selected = r.count() > 0;
                 dbits = __float_as_uint(dz);
                 Record R;
+                float tau, hx, hy;
+                cull_params(ca, cb, cc, op, (float)alpha_low, &tau, &hx, &hy);
                 R.a = make_float4(m2.x, m2.y, ca, cb);
                 R.b = make_float4(cc, op, c0f, c1f);
-                R.c = make_float4(c2f, 0.f, 0.f, 0.f);
+                R.c = make_float4(c2f, tau, hx, hy);
                 fused.rec[i] = R;
                 fused.gpack[i] = make_uint4((uint32_t)r.x0 | ((uint32_t)r.x1 << 16),
                                             (uint32_t)r.y0 | ((uint32_t)r.y1 << 16), 0u, __float_as_uint(dz));

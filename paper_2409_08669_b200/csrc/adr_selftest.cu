@@ -1,0 +1,62 @@
+// adr_selftest.cu — numerics self-tests exposed through the C ABI.
+//
+//   adr_exp_np_f32    : the render's float32 exp (numpy's AVX512F restatement)
+//                       on arbitrary inputs, for golden-vector tests.
+//   adr_selftest_exp  : exhaustive check that exp_np_fast (the render fast
+//                       path) equals exp_np on every float32 in [-87, 88].
+#include "adr_common.cuh"
+
+namespace adr {
+namespace {
+
+__global__ void k_exp_np(const float* __restrict__ x, float* __restrict__ y, int64_t n) {
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+        y[i] = exp_np(x[i]);
+}
+
+__global__ void k_selftest_exp(unsigned long long* mismatches, unsigned int* first_bad,
+                               unsigned long long* checked) {
+    unsigned long long bad = 0, seen = 0;
+    const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+    for (uint64_t u = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; u < (1ull << 32); u += stride) {
+        const float x = __uint_as_float((uint32_t)u);
+        if (!(x >= -87.0f && x <= 88.0f)) continue;
+        ++seen;
+        if (__float_as_uint(exp_np_fast(x)) != __float_as_uint(exp_np(x))) {
+            ++bad;
+            atomicMin(first_bad, (uint32_t)u);
+        }
+    }
+    if (bad) atomicAdd(mismatches, bad);
+    atomicAdd(checked, seen);
+}
+
+}  // namespace
+}  // namespace adr
+
+using namespace adr;
+
+extern "C" {
+
+int32_t adr_exp_np_f32(const float* d_x, float* d_y, int64_t n, void* stream) {
+    if (n <= 0) return ADR_OK;
+    const int64_t blocks = ceil_div(n, 256) < 4096 ? ceil_div(n, 256) : 4096;
+    k_exp_np<<<blocks, 256, 0, as_stream(stream)>>>(d_x, d_y, n);
+    ADR_LAUNCH_CHECK();
+    return ADR_OK;
+}
+
+int32_t adr_selftest_exp(uint64_t* d_result, void* stream) {
+    // d_result[0] = mismatches, d_result[1] = float inputs checked,
+    // d_result[2] (low 32 bits) = smallest mismatching bit pattern
+    cudaStream_t st = as_stream(stream);
+    ADR_CUDA_TRY(cudaMemsetAsync(d_result, 0, 2 * sizeof(uint64_t), st));
+    ADR_CUDA_TRY(cudaMemsetAsync(d_result + 2, 0xff, sizeof(uint64_t), st));
+    k_selftest_exp<<<148 * 8, 256, 0, st>>>(reinterpret_cast<unsigned long long*>(d_result),
+                                            reinterpret_cast<unsigned int*>(d_result + 2),
+                                            reinterpret_cast<unsigned long long*>(d_result + 1));
+    ADR_LAUNCH_CHECK();
+    return ADR_OK;
+}
+
+}  // extern "C"

@@ -190,6 +190,41 @@ def test_modes_lossless_and_pairs_monotone():
     assert res["aabb"].stats.pair_count <= res["circle"].stats.pair_count <= base.stats.pair_count
 
 
+# -- numerics pins -------------------------------------------------------------
+
+def test_gpu_exp_matches_numpy_golden_vectors():
+    """The render's float32 exp vs numpy's np.exp bits (tests/golden/exp_np_f32.npz)."""
+    import torch
+
+    from conftest import GOLDEN
+    from paper_2409_08669_b200 import _lib
+
+    with np.load(GOLDEN / "exp_np_f32.npz") as z:
+        x = z["x_bits"].view(np.float32)
+        y = z["y_bits"]
+    dx = torch.from_numpy(x.copy()).cuda()
+    dy = torch.empty_like(dx)
+    _lib.check(_lib.lib().adr_exp_np_f32(_lib.ptr(dx), _lib.ptr(dy), dx.numel(),
+                                         _lib.stream_handle(torch.cuda.current_stream())))
+    got = dy.cpu().numpy().view(np.uint32)
+    nan = np.isnan(y.view(np.float32))
+    assert np.array_equal(got[~nan], y[~nan])
+    assert np.all(np.isnan(got.view(np.float32)[nan]))
+
+
+def test_exp_fast_path_exhaustive():
+    """exp_np_fast == exp_np on every float32 in [-87, 88] (~2.2e9 inputs)."""
+    import torch
+
+    from paper_2409_08669_b200 import _lib
+
+    res = torch.zeros(3, dtype=torch.int64, device="cuda")
+    _lib.check(_lib.lib().adr_selftest_exp(_lib.ptr(res), _lib.stream_handle(torch.cuda.current_stream())))
+    mism, checked, first = res.cpu().tolist()
+    assert checked > 2_000_000_000
+    assert mism == 0, f"{mism} mismatches, first bit pattern {first & 0xffffffff:#010x}"
+
+
 # -- stage-API known answers (reference tests/test_tiling.py, test_render.py) ----
 
 def test_inclusive_sum_known_answers():
