@@ -33,6 +33,7 @@ struct FrameLayout {
     uint32_t* order;
     Record* rec;
     uint4* gpack;
+    uint32_t* tile_order;
     void* binning;
     size_t binning_bytes;
 };
@@ -44,6 +45,7 @@ size_t frame_bytes(int64_t n, int64_t n_tiles, int64_t cap, FrameLayout* out, vo
     l.order = c.take<uint32_t>(n);
     l.rec = c.take<Record>(n);
     l.gpack = c.take<uint4>(n);
+    l.tile_order = c.take<uint32_t>(n_tiles);
     l.binning_bytes = frame_binning_scratch(n, cap, n_tiles);
     l.binning = c.take<char>((int64_t)l.binning_bytes);
     if (out) *out = l;
@@ -193,6 +195,7 @@ int32_t adr_render_frame(const adr_scene* scene, const adr_camera* cam, int32_t 
     ra.rec = L.rec;
     ra.idx = reinterpret_cast<const uint32_t*>(buf->d_gidx);
     ra.ranges = buf->d_ranges;
+    ra.order = nullptr;  // longest-span-first order measured no gain (profiles/r01_notes.md)
     ra.width = cam->width;
     ra.height = cam->height;
     ra.tiles_x = tx;

@@ -18,29 +18,34 @@ struct __align__(16) Record {
 // alpha < alpha_low):
 //   tau      : power < tau  =>  alpha < alpha_low.  exp_np is within 2 ulp of
 //              exp and the product adds one rounding, so
-//              ln(alpha_low / sigma) - 1e-5 (rounded down) is a strict bound.
+//              ln(alpha_low / sigma) - 1e-5 (rounded down) is a strict bound;
+//              it is raised to -87 (sigma < 1e30 makes alpha < alpha_low there
+//              too), so every power the render evaluates lies in [-87, 0+].
+//              Special values:
+//                +inf : sigma <= 0 (or NaN) — the splat never contributes;
+//                -inf : "slow" splat — no tau culling and the full exp_np:
+//                       sigma >= 1e30 or non-finite, a colour non-finite, or
+//                       a conic that is not positive definite and well
+//                       conditioned (its fp32 power may exceed 88).
 //   (hx, hy) : every pixel with |px - mx| > hx or |py - my| > hy has
 //              power < tau *as computed in fp32*: the box of the ellipse
 //              Q(d) <= -2 tau, inflated by s = sqrt((1 + 1e-4) / (1 - eta))
 //              where eta bounds the relative fp32 evaluation error of power
 //              (8 ulp * (max|a|,|c| + |b|/2) / lambda_min), plus 1e-3 px.
-//              Non-positive-definite or ill-conditioned conics get an
-//              infinite box (no culling).
+//              Slow splats get an infinite box (no culling).
 // A contribution is only skipped when the reference provably skips it, so
 // the image and load map stay bit-identical.
-__device__ inline void cull_params(float a, float b, float c, float op, float alpha_low32, float* tau,
-                                            float* hx, float* hy) {
+__device__ inline void cull_params(float a, float b, float c, float op, float alpha_low32, float c0, float c1,
+                                   float c2, float* tau, float* hx, float* hy) {
     const float kInf = __int_as_float(0x7f800000);
     if (!(op > 0.0f)) {
         *tau = kInf;
         *hx = *hy = 0.0f;
         return;
     }
-    const double t = log((double)alpha_low32 / (double)op) - 1e-5;
-    const float t32 = __double2float_rd(t);
-    *tau = t32;
+    *tau = -kInf;
     *hx = *hy = kInf;
-    const double K = -2.0 * (double)t32;
+    if (!(op < 1e30f) || !isfinite(c0) || !isfinite(c1) || !isfinite(c2)) return;
     const double da = a, db = b, dc = c;
     const double det = da * dc - db * db;
     if (!(det > 0.0) || !(da > 0.0) || !(dc > 0.0)) return;
@@ -50,6 +55,11 @@ __device__ inline void cull_params(float a, float b, float c, float op, float al
     const double M = (da > dc ? da : dc) + 0.5 * fabs(db);
     const double eta = 2.0 * 8.0 * 5.9604644775390625e-08 * M / lmin;
     if (!(eta < 0.25)) return;
+    const double t = log((double)alpha_low32 / (double)op) - 1e-5;
+    float t32 = __double2float_rd(t);
+    t32 = t32 > -87.0f ? t32 : -87.0f;
+    *tau = t32;
+    const double K = -2.0 * (double)t32;
     if (K <= 0.0) {
         *hx = *hy = 1.0f;
         return;
@@ -77,6 +87,7 @@ struct RenderArgs {
     const Record* rec;        // records
     const uint32_t* idx;      // per sorted pair: record index
     const int64_t* ranges;    // (n_tiles, 2) int64 spans
+    uint32_t* order;          // scratch (n_tiles): tiles by decreasing span, or null
     int32_t width, height, tiles_x, tiles_y;
     float bg[3];
     float alpha_low;

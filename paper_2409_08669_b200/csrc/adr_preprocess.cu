@@ -243,7 +243,7 @@ k_preprocess(const T* __restrict__ centers, const T* __restrict__ scales,
                 dbits = __float_as_uint(dz);
                 Record R;
                 float tau, hx, hy;
-                cull_params(ca, cb, cc, op, (float)alpha_low, &tau, &hx, &hy);
+                cull_params(ca, cb, cc, op, (float)alpha_low, c0f, c1f, c2f, &tau, &hx, &hy);
                 R.a = make_float4(m2.x, m2.y, ca, cb);
                 R.b = make_float4(cc, op, c0f, c1f);
                 R.c = make_float4(c2f, tau, hx, hy);

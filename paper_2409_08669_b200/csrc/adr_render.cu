@@ -2,10 +2,15 @@
 // blending and the per-pixel load map, with the load-statistics epilogue
 // (LoadStats / load_loss, sb/metrics.py:59-86).
 //
-// One CTA per 16x16 tile, one thread per pixel.  Each batch of 256 pairs is
-// gathered into shared memory; every pixel then walks the batch in order with
-// the exact fp32 recurrence of SURVEY.md App. A.3 (numpy float32 exp, no FMA
-// contraction), so the image and load map equal the reference bit for bit.
+// One CTA (128 threads) per 16x16 tile; each thread owns two horizontally
+// adjacent pixels and evaluates them together in packed fp32x2 arithmetic
+// (FADD2/FMUL2/FFMA2: two IEEE round-to-nearest ops per instruction, see
+// adr_f32x2.cuh), which halves the issue slots of the exact blend.  Each batch
+// of 256 pairs is gathered into shared memory; every pixel walks the batch in
+// order with the exact fp32 recurrence of SURVEY.md App. A.3 (numpy float32
+// exp, no FMA contraction), so the image and load map equal the reference bit
+// for bit.
+#include "adr_f32x2.cuh"
 #include "adr_kernels.cuh"
 #include "adr_scan.cuh"
 
@@ -13,7 +18,8 @@ namespace adr {
 
 namespace {
 
-constexpr int kRenderBlock = kTilePixels;  // 256
+constexpr int kRenderThreads = 128;       // 2 pixels per thread
+constexpr int kBatch = 256;               // pairs staged per round
 
 // Record source for the fused frame: records by rank + per-pair rank list.
 struct RecSource {
@@ -35,131 +41,195 @@ struct ProjSource {
         const float2 m = mean2d[g];
         Record r;
         const float a = conic[3 * g], b = conic[3 * g + 1], c = conic[3 * g + 2], op = opacity[g];
+        const float c0 = color[3 * g], c1 = color[3 * g + 1], c2 = color[3 * g + 2];
         float tau, hx, hy;
-        cull_params(a, b, c, op, alpha_low, &tau, &hx, &hy);
+        cull_params(a, b, c, op, alpha_low, c0, c1, c2, &tau, &hx, &hy);
         r.a = make_float4(m.x, m.y, a, b);
-        r.b = make_float4(c, op, color[3 * g], color[3 * g + 1]);
-        r.c = make_float4(color[3 * g + 2], tau, hx, hy);
+        r.b = make_float4(c, op, c0, c1);
+        r.c = make_float4(c2, tau, hx, hy);
         return r;
     }
 };
 
-// Rows 2w, 2w+1 of the tile belong to warp w: bit w of the mask is set when
+// Rows 4w .. 4w+3 of the tile belong to warp w: bit w of the mask is set when
 // the splat's conservative box (mx +- hx, my +- hy) meets those pixel rows
 // and the tile's pixel columns.
 __device__ __forceinline__ uint32_t warp_mask(const Record& r, float x_lo, float y_lo) {
     const float mx = r.a.x, my = r.a.y, hx = r.c.z, hy = r.c.w;
     if (!(mx - hx <= x_lo + (kTile - 1)) || !(mx + hx >= x_lo)) return 0u;
-    const float lo = fmaxf(fminf(ceilf(0.5f * ((my - hy) - y_lo - 1.0f)), 8.0f), 0.0f);
-    const float hi = fmaxf(fminf(floorf(0.5f * ((my + hy) - y_lo)), 7.0f), -1.0f);
+    const float lo = fmaxf(fminf(ceilf(0.25f * ((my - hy) - y_lo - 3.0f)), 4.0f), 0.0f);
+    const float hi = fmaxf(fminf(floorf(0.25f * ((my + hy) - y_lo)), 3.0f), -1.0f);
     const int w0 = (int)lo, w1 = (int)hi;
     if (w1 < w0) return 0u;
     return ((2u << w1) - 1u) & ~((1u << w0) - 1u);
 }
 
+// One pixel's blend step with the full exp_np (slow splats).
+__device__ __forceinline__ void blend_scalar(float fpx, float fpy, const float4& G, const float2& Tc, const float4& W,
+                                             float alpha_low, float term, float& T, float& C0, float& C1, float& C2,
+                                             int& cnt, bool& done) {
+    if (done) return;
+    const float dx = __fsub_rn(fpx, G.x);
+    const float dy = __fsub_rn(fpy, G.y);
+    const float q = __fadd_rn(__fmul_rn(__fmul_rn(G.z, dx), dx), __fmul_rn(__fmul_rn(Tc.x, dy), dy));
+    const float power = __fsub_rn(__fmul_rn(-0.5f, q), __fmul_rn(__fmul_rn(G.w, dx), dy));
+    if (power < Tc.y) return;
+    const float e = (power >= -87.0f && power <= 88.0f) ? exp_np_fast(power) : exp_np(power);
+    float alpha = __fmul_rn(W.x, e);
+    alpha = alpha < 0.99f ? alpha : (alpha != alpha ? alpha : 0.99f);
+    if (!(alpha >= alpha_low)) return;
+    const float w = __fmul_rn(alpha, T);
+    C0 = __fadd_rn(C0, __fmul_rn(w, W.y));
+    C1 = __fadd_rn(C1, __fmul_rn(w, W.z));
+    C2 = __fadd_rn(C2, __fmul_rn(w, W.w));
+    T = __fmul_rn(T, __fsub_rn(1.0f, alpha));
+    ++cnt;
+    if (T < term) done = true;
+}
+
 template <class Src>
-__global__ void __launch_bounds__(kRenderBlock)
+__global__ void __launch_bounds__(kRenderThreads)
 k_render(Src src, const int64_t* __restrict__ ranges, int32_t width, int32_t height, int32_t tiles_x, float bg0,
          float bg1, float bg2, float alpha_low, float term, float* __restrict__ pixels, int32_t* __restrict__ load,
-         adr_load_stats* stats, int32_t* hist, int32_t hist_bins) {
+         adr_load_stats* stats, int32_t* hist, int32_t hist_bins, F2K K, const uint32_t* __restrict__ order) {
     // shared-memory batch, split by use: the power test needs (mx, my, a, b)
-    // + (c, tau); only contributions that pass it read (sigma, r, g, b)
-    __shared__ float4 sG[kRenderBlock];   // mx, my, a, b
-    __shared__ float2 sT[kRenderBlock];   // c, tau
-    __shared__ float4 sW[kRenderBlock];   // sigma, r, g, b
-    __shared__ uint8_t smask[kRenderBlock];
-    __shared__ unsigned long long ssum[kRenderBlock / 32], ssq[kRenderBlock / 32];
-    __shared__ int smin[kRenderBlock / 32], smax[kRenderBlock / 32];
-    const int tile = blockIdx.x;
+    // + (c, tau); only splats that pass it read (sigma, r, g, b)
+    __shared__ float4 sG[kBatch];   // mx, my, a, b
+    __shared__ float2 sT[kBatch];   // c, tau
+    __shared__ float4 sW[kBatch];   // sigma, r, g, b
+    __shared__ uint8_t smask[kBatch];
+    __shared__ unsigned long long ssum[kRenderThreads / 32], ssq[kRenderThreads / 32];
+    __shared__ int smin[kRenderThreads / 32], smax[kRenderThreads / 32];
+    const int tile = order ? (int)order[blockIdx.x] : (int)blockIdx.x;
     const int ty = tile / tiles_x, tx = tile - ty * tiles_x;
-    const int px = tx * kTile + (threadIdx.x & (kTile - 1));
-    const int py = ty * kTile + (threadIdx.x >> 4);
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const bool inside = px < width && py < height;
+    const int px0 = tx * kTile + 2 * (lane & 7);
+    const int py = ty * kTile + 4 * warp + (lane >> 3);
+    const bool in0 = px0 < width && py < height, in1 = px0 + 1 < width && py < height;
     const int64_t start = ranges[2 * tile], end = ranges[2 * tile + 1];
-    const float fpx = (float)px, fpy = (float)py;
+    const float fpx0 = (float)px0, fpx1 = (float)(px0 + 1), fpy = (float)py;
+    const f2 PX = pk(fpx0, fpx1);
     const float x_lo = (float)(tx * kTile), y_lo = (float)(ty * kTile);
 
-    float T = 1.0f, C0 = 0.0f, C1 = 0.0f, C2 = 0.0f;
-    int cnt = 0;
-    bool done = !inside;
-    for (int64_t b = start; b < end; b += kRenderBlock) {
-        if (__syncthreads_count(done) == kRenderBlock) break;
-        const int nb = (int)((end - b) < kRenderBlock ? (end - b) : kRenderBlock);
-        if ((int)threadIdx.x < nb) {
-            const Record r = src.load(b + threadIdx.x);
-            sG[threadIdx.x] = r.a;
-            sT[threadIdx.x] = make_float2(r.b.x, r.c.y);
-            sW[threadIdx.x] = make_float4(r.b.y, r.b.z, r.b.w, r.c.x);
-            smask[threadIdx.x] = (uint8_t)warp_mask(r, x_lo, y_lo);
+    f2 T = K.one, C0 = 0ull, C1 = 0ull, C2 = 0ull;  // (+0, +0)
+    int cnt0 = 0, cnt1 = 0;
+    bool done0 = !in0, done1 = !in1;
+    for (int64_t b = start; b < end; b += kBatch) {
+        if (__syncthreads_count(done0 && done1) == kRenderThreads) break;
+        const int nb = (int)((end - b) < kBatch ? (end - b) : kBatch);
+        for (int i = threadIdx.x; i < nb; i += kRenderThreads) {
+            const Record r = src.load(b + i);
+            sG[i] = r.a;
+            sT[i] = make_float2(r.b.x, r.c.y);
+            sW[i] = make_float4(r.b.y, r.b.z, r.b.w, r.c.x);
+            smask[i] = (uint8_t)warp_mask(r, x_lo, y_lo);
         }
         __syncthreads();
-        if (__any_sync(kFull, !done)) {
+        if (__any_sync(kFull, !(done0 && done1))) {
             for (int c0 = 0; c0 < nb; c0 += 32) {
                 uint32_t m = __ballot_sync(kFull, c0 + lane < nb && ((smask[c0 + lane] >> warp) & 1u));
                 while (m) {
                     const int j = c0 + __ffs(m) - 1;
                     m &= m - 1u;
-                    if (done) continue;
+                    if (done0 && done1) continue;
                     const float4 G = sG[j];
                     const float2 Tc = sT[j];
-                    const float dx = __fsub_rn(fpx, G.x);
+                    const float tau = Tc.y;
+                    if (tau < -3.0e38f) {  // slow splat: full exp_np, scalar per pixel
+                        const float4 W = sW[j];
+                        float t0 = lo_of(T), t1 = hi_of(T);
+                        float a0 = lo_of(C0), a1 = hi_of(C0), b0 = lo_of(C1), b1 = hi_of(C1);
+                        float d0 = lo_of(C2), d1 = hi_of(C2);
+                        blend_scalar(fpx0, fpy, G, Tc, W, alpha_low, term, t0, a0, b0, d0, cnt0, done0);
+                        blend_scalar(fpx1, fpy, G, Tc, W, alpha_low, term, t1, a1, b1, d1, cnt1, done1);
+                        T = pk(t0, t1);
+                        C0 = pk(a0, a1);
+                        C1 = pk(b0, b1);
+                        C2 = pk(d0, d1);
+                        continue;
+                    }
+                    // power = (-0.5 * ((a*dx)*dx + (c*dy)*dy)) - ((b*dx)*dy), both lanes
                     const float dy = __fsub_rn(fpy, G.y);
-                    const float q = __fadd_rn(__fmul_rn(__fmul_rn(G.z, dx), dx), __fmul_rn(__fmul_rn(Tc.x, dy), dy));
-                    const float power = __fsub_rn(__fmul_rn(-0.5f, q), __fmul_rn(__fmul_rn(G.w, dx), dy));
-                    if (power < Tc.y) continue;  // alpha < alpha_low for sure (cull_params)
+                    const float cdd = __fmul_rn(__fmul_rn(Tc.x, dy), dy);
+                    const f2 dx = sub2(PX, bc(G.x), K);
+                    const f2 q = add2(mul2(mul2(bc(G.z), dx, K), dx, K), bc(cdd), K);
+                    const f2 bd = mul2(mul2(bc(G.w), dx, K), bc(dy), K);
+                    const f2 pw = sub2(mul2(bc(-0.5f), q, K), bd, K);
+                    bool p0 = !done0 && lo_of(pw) >= tau;
+                    bool p1 = !done1 && hi_of(pw) >= tau;
+                    if (!(p0 || p1)) continue;  // both alphas < alpha_low for sure
                     const float4 W = sW[j];
-                    const float e = (power >= -87.0f && power <= 88.0f) ? exp_np_fast(power) : exp_np(power);
-                    float alpha = __fmul_rn(W.x, e);
-                    alpha = alpha < 0.99f ? alpha : (alpha != alpha ? alpha : 0.99f);
-                    if (!(alpha >= alpha_low)) continue;
-                    const float w = __fmul_rn(alpha, T);
-                    C0 = __fadd_rn(C0, __fmul_rn(w, W.y));
-                    C1 = __fadd_rn(C1, __fmul_rn(w, W.z));
-                    C2 = __fadd_rn(C2, __fmul_rn(w, W.w));
-                    T = __fmul_rn(T, __fsub_rn(1.0f, alpha));
-                    ++cnt;
-                    if (T < term) done = true;
+                    const f2 al = mul2(bc(W.x), exp2_np_fast(pw, K), K);
+                    float a0 = fminf(lo_of(al), 0.99f), a1 = fminf(hi_of(al), 0.99f);  // finite here
+                    p0 = p0 && a0 >= alpha_low;
+                    p1 = p1 && a1 >= alpha_low;
+                    if (!(p0 || p1)) continue;
+                    // a lane that does not contribute blends alpha = 0 — an exact
+                    // no-op (T * 1 = T, C + 0 * colour = C for finite colours),
+                    // which is also what the reference does (render.py:98-109)
+                    const f2 A = pk(p0 ? a0 : 0.0f, p1 ? a1 : 0.0f);
+                    const f2 w = mul2(A, T, K);
+                    C0 = add2(C0, mul2(w, bc(W.y), K), K);
+                    C1 = add2(C1, mul2(w, bc(W.z), K), K);
+                    C2 = add2(C2, mul2(w, bc(W.w), K), K);
+                    T = mul2(T, sub2(K.one, A, K), K);
+                    cnt0 += p0;
+                    cnt1 += p1;
+                    if (p0 && lo_of(T) < term) done0 = true;
+                    if (p1 && hi_of(T) < term) done1 = true;
                 }
-                if (__all_sync(kFull, done)) break;
+                if (__all_sync(kFull, done0 && done1)) break;
             }
         }
     }
-    if (inside) {
-        const int64_t pix = (int64_t)py * width + px;
-        float o0 = __fadd_rn(C0, __fmul_rn(T, bg0));
-        float o1 = __fadd_rn(C1, __fmul_rn(T, bg1));
-        float o2 = __fadd_rn(C2, __fmul_rn(T, bg2));
-        o0 = o0 < 0.f ? 0.f : (o0 > 1.f ? 1.f : o0);
-        o1 = o1 < 0.f ? 0.f : (o1 > 1.f ? 1.f : o1);
-        o2 = o2 < 0.f ? 0.f : (o2 > 1.f ? 1.f : o2);
-        pixels[3 * pix] = o0;
-        pixels[3 * pix + 1] = o1;
-        pixels[3 * pix + 2] = o2;
-        load[pix] = cnt;
-        if (hist) atomicAdd(hist + (cnt < hist_bins ? cnt : hist_bins - 1), 1);
+    const float t0 = lo_of(T), t1 = hi_of(T);
+    const float o[2][3] = {{__fadd_rn(lo_of(C0), __fmul_rn(t0, bg0)), __fadd_rn(lo_of(C1), __fmul_rn(t0, bg1)),
+                            __fadd_rn(lo_of(C2), __fmul_rn(t0, bg2))},
+                           {__fadd_rn(hi_of(C0), __fmul_rn(t1, bg0)), __fadd_rn(hi_of(C1), __fmul_rn(t1, bg1)),
+                            __fadd_rn(hi_of(C2), __fmul_rn(t1, bg2))}};
+    const bool ins[2] = {in0, in1};
+    const int cnts[2] = {cnt0, cnt1};
+#pragma unroll
+    for (int k = 0; k < 2; ++k) {
+        if (!ins[k]) continue;
+        const int64_t pix = (int64_t)py * width + px0 + k;
+#pragma unroll
+        for (int ch = 0; ch < 3; ++ch) {
+            const float v = o[k][ch];
+            pixels[3 * pix + ch] = v < 0.f ? 0.f : (v > 1.f ? 1.f : v);
+        }
+        load[pix] = cnts[k];
+        if (hist) atomicAdd(hist + (cnts[k] < hist_bins ? cnts[k] : hist_bins - 1), 1);
     }
     if (stats) {
-        unsigned long long s = inside ? (unsigned long long)cnt : 0ull;
-        unsigned long long s2 = inside ? (unsigned long long)cnt * (unsigned long long)cnt : 0ull;
-        int mn = inside ? cnt : INT_MAX, mx = inside ? cnt : INT_MIN;
-#pragma unroll
-        for (int o = 16; o > 0; o >>= 1) {
-            s += __shfl_xor_sync(kFull, s, o);
-            s2 += __shfl_xor_sync(kFull, s2, o);
-            mn = min(mn, __shfl_xor_sync(kFull, mn, o));
-            mx = max(mx, __shfl_xor_sync(kFull, mx, o));
+        unsigned long long s = (in0 ? (unsigned long long)cnt0 : 0ull) + (in1 ? (unsigned long long)cnt1 : 0ull);
+        unsigned long long s2 = (in0 ? (unsigned long long)cnt0 * (unsigned long long)cnt0 : 0ull) +
+                                (in1 ? (unsigned long long)cnt1 * (unsigned long long)cnt1 : 0ull);
+        int mn = INT_MAX, mx = INT_MIN;
+        if (in0) {
+            mn = min(mn, cnt0);
+            mx = max(mx, cnt0);
         }
-        const int w = threadIdx.x >> 5;
-        if ((threadIdx.x & 31) == 0) {
-            ssum[w] = s;
-            ssq[w] = s2;
-            smin[w] = mn;
-            smax[w] = mx;
+        if (in1) {
+            mn = min(mn, cnt1);
+            mx = max(mx, cnt1);
+        }
+#pragma unroll
+        for (int o2 = 16; o2 > 0; o2 >>= 1) {
+            s += __shfl_xor_sync(kFull, s, o2);
+            s2 += __shfl_xor_sync(kFull, s2, o2);
+            mn = min(mn, __shfl_xor_sync(kFull, mn, o2));
+            mx = max(mx, __shfl_xor_sync(kFull, mx, o2));
+        }
+        if (lane == 0) {
+            ssum[warp] = s;
+            ssq[warp] = s2;
+            smin[warp] = mn;
+            smax[warp] = mx;
         }
         __syncthreads();
         if (threadIdx.x == 0) {
-            for (int k = 1; k < kRenderBlock / 32; ++k) {
+            for (int k = 1; k < kRenderThreads / 32; ++k) {
                 s += ssum[k];
                 s2 += ssq[k];
                 mn = min(mn, smin[k]);
@@ -170,6 +240,35 @@ k_render(Src src, const int64_t* __restrict__ ranges, int32_t width, int32_t hei
             atomicMin(&stats->min, mn);
             atomicMax(&stats->max, mx);
         }
+    }
+}
+
+// Longest-span-first launch order of the tiles (LPT scheduling): tiles are
+// bucketed by floor(log2(span + 1)), heaviest bucket first, so the heavy
+// tiles of the image centre start in the first wave instead of forming the
+// tail.  Order within a bucket is arbitrary; every tile's output depends only
+// on its own span, so results are unaffected.
+__global__ void __launch_bounds__(1024) k_tile_order(const int64_t* __restrict__ ranges, int32_t n_tiles,
+                                                     uint32_t* __restrict__ order) {
+    __shared__ uint32_t cnt[64], pos[64];
+    if (threadIdx.x < 64) cnt[threadIdx.x] = 0;
+    __syncthreads();
+    for (int t = threadIdx.x; t < n_tiles; t += blockDim.x) {
+        const uint64_t len = (uint64_t)(ranges[2 * t + 1] - ranges[2 * t]);
+        atomicAdd(&cnt[__clzll(len + 1)], 1u);
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        uint32_t s = 0;
+        for (int k = 0; k < 64; ++k) {
+            pos[k] = s;
+            s += cnt[k];
+        }
+    }
+    __syncthreads();
+    for (int t = threadIdx.x; t < n_tiles; t += blockDim.x) {
+        const uint64_t len = (uint64_t)(ranges[2 * t + 1] - ranges[2 * t]);
+        order[atomicAdd(&pos[__clzll(len + 1)], 1u)] = (uint32_t)t;
     }
 }
 
@@ -199,9 +298,13 @@ int32_t launch_render(const RenderArgs& a, cudaStream_t st) {
     const int64_t n_tiles = (int64_t)a.tiles_x * a.tiles_y;
     if (n_tiles <= 0) return ADR_OK;
     RecSource src{a.rec, a.idx};
-    k_render<RecSource><<<n_tiles, kRenderBlock, 0, st>>>(src, a.ranges, a.width, a.height, a.tiles_x, a.bg[0], a.bg[1],
-                                                         a.bg[2], a.alpha_low, a.term, a.pixels, a.load, a.stats,
-                                                         a.hist, a.hist_bins);
+    if (a.order) {
+        k_tile_order<<<1, 1024, 0, st>>>(a.ranges, (int32_t)n_tiles, a.order);
+        ADR_LAUNCH_CHECK();
+    }
+    k_render<RecSource><<<n_tiles, kRenderThreads, 0, st>>>(src, a.ranges, a.width, a.height, a.tiles_x, a.bg[0], a.bg[1],
+                                                           a.bg[2], a.alpha_low, a.term, a.pixels, a.load, a.stats,
+                                                           a.hist, a.hist_bins, f2k_host(), a.order);
     ADR_LAUNCH_CHECK();
     return ADR_OK;
 }
@@ -213,8 +316,8 @@ int32_t launch_render_proj(const adr_projection& p, const int64_t* gidx, const i
     const int64_t n_tiles = (int64_t)tx * ty;
     if (n_tiles <= 0) return ADR_OK;
     ProjSource src{reinterpret_cast<const float2*>(p.d_mean2d), p.d_conic, p.d_opacity, p.d_color, gidx, alpha_low};
-    k_render<ProjSource><<<n_tiles, kRenderBlock, 0, st>>>(src, ranges, width, height, tx, bg[0], bg[1], bg[2],
-                                                          alpha_low, term, pixels, load, stats, hist, bins);
+    k_render<ProjSource><<<n_tiles, kRenderThreads, 0, st>>>(src, ranges, width, height, tx, bg[0], bg[1], bg[2],
+                                                            alpha_low, term, pixels, load, stats, hist, bins, f2k_host(), nullptr);
     ADR_LAUNCH_CHECK();
     return ADR_OK;
 }

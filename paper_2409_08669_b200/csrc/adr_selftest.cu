@@ -2,9 +2,12 @@
 //
 //   adr_exp_np_f32    : the render's float32 exp (numpy's AVX512F restatement)
 //                       on arbitrary inputs, for golden-vector tests.
-//   adr_selftest_exp  : exhaustive check that exp_np_fast (the render fast
-//                       path) equals exp_np on every float32 in [-87, 88].
+//   adr_selftest_exp  : exhaustive check that exp_np_fast and the packed
+//                       exp2_np_fast (both render fast paths; the packed one
+//                       evaluated with a different partner value in the other
+//                       lane) equal exp_np on every float32 in [-87, 88].
 #include "adr_common.cuh"
+#include "adr_f32x2.cuh"
 
 namespace adr {
 namespace {
@@ -15,14 +18,18 @@ __global__ void k_exp_np(const float* __restrict__ x, float* __restrict__ y, int
 }
 
 __global__ void k_selftest_exp(unsigned long long* mismatches, unsigned int* first_bad,
-                               unsigned long long* checked) {
+                               unsigned long long* checked, F2K k) {
     unsigned long long bad = 0, seen = 0;
     const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
     for (uint64_t u = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; u < (1ull << 32); u += stride) {
         const float x = __uint_as_float((uint32_t)u);
         if (!(x >= -87.0f && x <= 88.0f)) continue;
         ++seen;
-        if (__float_as_uint(exp_np_fast(x)) != __float_as_uint(exp_np(x))) {
+        const float partner = __fmul_rn(-0.5f, x);  // also in [-87, 88]
+        const f2 v = exp2_np_fast(pk(x, partner), k);
+        const uint32_t ref = __float_as_uint(exp_np(x));
+        if (__float_as_uint(exp_np_fast(x)) != ref || __float_as_uint(lo_of(v)) != ref ||
+            __float_as_uint(hi_of(v)) != __float_as_uint(exp_np(partner))) {
             ++bad;
             atomicMin(first_bad, (uint32_t)u);
         }
@@ -54,7 +61,7 @@ int32_t adr_selftest_exp(uint64_t* d_result, void* stream) {
     ADR_CUDA_TRY(cudaMemsetAsync(d_result + 2, 0xff, sizeof(uint64_t), st));
     k_selftest_exp<<<148 * 8, 256, 0, st>>>(reinterpret_cast<unsigned long long*>(d_result),
                                             reinterpret_cast<unsigned int*>(d_result + 2),
-                                            reinterpret_cast<unsigned long long*>(d_result + 1));
+                                            reinterpret_cast<unsigned long long*>(d_result + 1), f2k_host());
     ADR_LAUNCH_CHECK();
     return ADR_OK;
 }
