@@ -15,6 +15,9 @@ from .projection import (ALPHA_LOW, BASE_RADIUS_MULTIPLIER, COV_DILATION, FOV_CL
 from .render import ALPHA_CLAMP, TERMINATION_THRESHOLD, Image, LoadMap, render
 from .scene import (Camera, DeviceScene, Gaussian3D, Scene, SceneArrays, SyntheticSpec,
                     generate_synthetic, synthetic_arrays)
+from .scene_io import (SceneDiagnostic, load_json, load_ply, load_ply_arrays, load_scene,
+                       load_scene_arrays, normalize_quaternion, save_json, save_ply, save_scene,
+                       validate_scene)
 from .tiling import (TILE_SIZE, TileGrid, TilePairList, TileRect, build_pairs,
                      duplicate_with_keys, identify_tile_ranges, inclusive_sum, sort_pairs,
                      tiles_touched, touched_counts)
@@ -27,7 +30,9 @@ __all__ = [
     "CapacityError", "CullingMode", "DeviceScene", "Gaussian3D", "Image", "InternalError",
     "LoadMap", "LoadStats", "PipelineResult", "Projection", "Rasterizer", "RenderStats", "Scene",
     "SceneArrays", "SceneFormatError", "SceneValidationError", "SyntheticSpec", "TileGrid",
-    "TilePairList", "TileRect", "build_pairs", "duplicate_with_keys", "generate_synthetic",
+    "TilePairList", "TileRect", "build_pairs", "SceneDiagnostic", "load_json", "load_ply",
+    "load_ply_arrays", "load_scene", "load_scene_arrays", "normalize_quaternion", "save_json",
+    "save_ply", "save_scene", "validate_scene", "duplicate_with_keys", "generate_synthetic",
     "identify_tile_ranges", "inclusive_sum", "load_loss", "preprocess", "psnr", "render",
     "run_pipeline", "sort_pairs", "synthetic_arrays", "tiles_touched", "touched_counts",
 ]
