@@ -165,6 +165,20 @@ int32_t adr_exp_np_f32(const float* d_x, float* d_y, int64_t n, void* stream);
  * checked, d_result[2] = smallest mismatching bit pattern (all-ones if none). */
 int32_t adr_selftest_exp(uint64_t* d_result, void* stream);
 
+/* ------------------------------------------------- load-balancing objective */
+
+/* Image terms of total_loss (sb/metrics.py:94-143) in fp64: d_out[0] =
+ * l1_loss(a, b) (mean |a - b| over H*W*3), d_out[1] = ssim(a, b) (11-tap
+ * Gaussian window given in h_window — the host computes it with the
+ * reference's numpy expression, sb/metrics.py:108-111 — applied as
+ * scipy.ndimage.correlate1d along rows then columns with zero padding; SSIM
+ * constants c1, c2).  a, b: (H,W,3) float32 device images.  Asynchronous;
+ * scratch from adr_image_loss_scratch_bytes(). */
+size_t adr_image_loss_scratch_bytes(int32_t width, int32_t height);
+int32_t adr_image_losses(const float* d_a, const float* d_b, int32_t width, int32_t height,
+                         const double* h_window, double c1, double c2, double* d_out,
+                         void* d_scratch, size_t scratch_bytes, void* stream);
+
 /* --------------------------------------------- fused pipeline (run_pipeline)
  * sb/pipeline.py:85-124.  The frame runs as a fixed kernel sequence with no
  * host synchronisation, so it can be captured into a CUDA graph.  Pair

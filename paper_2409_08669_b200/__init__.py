@@ -8,7 +8,9 @@ exceptions, backed by hand-written sm_100a kernels in libadrsplat.so
 """
 
 from .errors import CapacityError, InternalError, SceneFormatError, SceneValidationError
-from .metrics import PSNR_IDENTICAL_SENTINEL, LoadStats, load_loss, psnr
+from .metrics import (DEFAULT_WEIGHTS, PSNR_IDENTICAL_SENTINEL, BalanceStepResult, LoadStats,
+                      LossWeights, l1_loss, load_loss, psnr, replace_opacity, ssim, toy_balance_step,
+                      total_loss)
 from .pipeline import STAGE_NAMES, PipelineResult, Rasterizer, RenderStats, run_pipeline
 from .projection import (ALPHA_LOW, BASE_RADIUS_MULTIPLIER, COV_DILATION, FOV_CLAMP_FACTOR,
                          CullingMode, Projection, preprocess)
@@ -32,7 +34,8 @@ __all__ = [
     "SceneArrays", "SceneFormatError", "SceneValidationError", "SyntheticSpec", "TileGrid",
     "TilePairList", "TileRect", "build_pairs", "SceneDiagnostic", "load_json", "load_ply",
     "load_ply_arrays", "load_scene", "load_scene_arrays", "normalize_quaternion", "save_json",
-    "save_ply", "save_scene", "validate_scene", "duplicate_with_keys", "generate_synthetic",
+    "save_ply", "save_scene", "validate_scene", "DEFAULT_WEIGHTS", "BalanceStepResult", "LossWeights",
+    "l1_loss", "replace_opacity", "ssim", "toy_balance_step", "total_loss", "duplicate_with_keys", "generate_synthetic",
     "identify_tile_ranges", "inclusive_sum", "load_loss", "preprocess", "psnr", "render",
     "run_pipeline", "sort_pairs", "synthetic_arrays", "tiles_touched", "touched_counts",
 ]

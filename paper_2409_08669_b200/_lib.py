@@ -31,7 +31,7 @@ EXPORTED = (
     "adr_touched_counts", "adr_inclusive_sum_scratch_bytes", "adr_inclusive_sum",
     "adr_duplicate_with_keys", "adr_sort_pairs_scratch_bytes", "adr_sort_pairs",
     "adr_identify_tile_ranges", "adr_render", "adr_exp_np_f32", "adr_selftest_exp",
-    "adr_frame_scratch_bytes", "adr_render_frame",
+    "adr_frame_scratch_bytes", "adr_render_frame", "adr_image_loss_scratch_bytes", "adr_image_losses",
 )
 
 
@@ -115,6 +115,8 @@ def lib() -> ctypes.CDLL:
             "adr_frame_scratch_bytes": (sz, [i64, i32, i32, i64]),
             "adr_render_frame": (i32, [P(Scene_t), P(Camera_t), i32, dbl, dbl, dbl,
                                        P(FrameBuffers_t), vp]),
+            "adr_image_loss_scratch_bytes": (sz, [i32, i32]),
+            "adr_image_losses": (i32, [vp, vp, i32, i32, P(dbl), dbl, dbl, vp, vp, sz, vp]),
         }
         for name, (res, args) in sigs.items():
             fn = getattr(L, name)
