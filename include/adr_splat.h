@@ -165,6 +165,20 @@ int32_t adr_exp_np_f32(const float* d_x, float* d_y, int64_t n, void* stream);
  * checked, d_result[2] = smallest mismatching bit pattern (all-ones if none). */
 int32_t adr_selftest_exp(uint64_t* d_result, void* stream);
 
+/* ----------------------------------------------- brute-force reference path */
+
+/* render_reference (sb/oracle.py:23-78) on the GPU: given a BASELINE-mode
+ * Projection of n Gaussians, sort the valid ones globally by (float32 depth
+ * bits, index) and blend every pixel over the Gaussians whose footprint
+ * rectangle overlaps its tile, with no tile binning.  Writes the (H,W,3)
+ * image and (H,W) load map; bit-identical to adr_render_frame's when stages
+ * 2-5 are correct.  Asynchronous; scratch from
+ * adr_render_reference_scratch_bytes(n). */
+size_t adr_render_reference_scratch_bytes(int64_t n);
+int32_t adr_render_reference(const adr_projection* proj, int64_t n, const adr_camera* cam,
+                             double alpha_low, double term_threshold, float* d_pixels,
+                             int32_t* d_load, void* d_scratch, size_t scratch_bytes, void* stream);
+
 /* ------------------------------------------------- load-balancing objective */
 
 /* Image terms of total_loss (sb/metrics.py:94-143) in fp64: d_out[0] =

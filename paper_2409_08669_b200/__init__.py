@@ -14,6 +14,7 @@ from .metrics import (DEFAULT_WEIGHTS, PSNR_IDENTICAL_SENTINEL, BalanceStepResul
 from .pipeline import STAGE_NAMES, PipelineResult, Rasterizer, RenderStats, run_pipeline
 from .projection import (ALPHA_LOW, BASE_RADIUS_MULTIPLIER, COV_DILATION, FOV_CLAMP_FACTOR,
                          CullingMode, Projection, preprocess)
+from .refrender import render_reference
 from .render import ALPHA_CLAMP, TERMINATION_THRESHOLD, Image, LoadMap, render
 from .scene import (Camera, DeviceScene, Gaussian3D, Scene, SceneArrays, SyntheticSpec,
                     generate_synthetic, synthetic_arrays)
@@ -35,7 +36,7 @@ __all__ = [
     "TilePairList", "TileRect", "build_pairs", "SceneDiagnostic", "load_json", "load_ply",
     "load_ply_arrays", "load_scene", "load_scene_arrays", "normalize_quaternion", "save_json",
     "save_ply", "save_scene", "validate_scene", "DEFAULT_WEIGHTS", "BalanceStepResult", "LossWeights",
-    "l1_loss", "replace_opacity", "ssim", "toy_balance_step", "total_loss", "duplicate_with_keys", "generate_synthetic",
+    "l1_loss", "render_reference", "replace_opacity", "ssim", "toy_balance_step", "total_loss", "duplicate_with_keys", "generate_synthetic",
     "identify_tile_ranges", "inclusive_sum", "load_loss", "preprocess", "psnr", "render",
     "run_pipeline", "sort_pairs", "synthetic_arrays", "tiles_touched", "touched_counts",
 ]

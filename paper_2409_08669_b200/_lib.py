@@ -32,6 +32,7 @@ EXPORTED = (
     "adr_duplicate_with_keys", "adr_sort_pairs_scratch_bytes", "adr_sort_pairs",
     "adr_identify_tile_ranges", "adr_render", "adr_exp_np_f32", "adr_selftest_exp",
     "adr_frame_scratch_bytes", "adr_render_frame", "adr_image_loss_scratch_bytes", "adr_image_losses",
+    "adr_render_reference_scratch_bytes", "adr_render_reference",
 )
 
 
@@ -117,6 +118,8 @@ def lib() -> ctypes.CDLL:
                                        P(FrameBuffers_t), vp]),
             "adr_image_loss_scratch_bytes": (sz, [i32, i32]),
             "adr_image_losses": (i32, [vp, vp, i32, i32, P(dbl), dbl, dbl, vp, vp, sz, vp]),
+            "adr_render_reference_scratch_bytes": (sz, [i64]),
+            "adr_render_reference": (i32, [P(Projection_t), i64, P(Camera_t), dbl, dbl, vp, vp, vp, sz, vp]),
         }
         for name, (res, args) in sigs.items():
             fn = getattr(L, name)

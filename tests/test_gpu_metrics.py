@@ -74,3 +74,44 @@ def test_toy_balance_step_matches_reference(toy):
     print(f"toy step: GPU {dt * 1e3:.1f} ms vs reference {float(toy['toy_ref_seconds']) * 1e3:.0f} ms (CPU)")
     with pytest.raises(ValueError):
         ab.toy_balance_step(scene, cam, reference, ab.LossWeights(), step=0.0)
+
+
+# -- brute-force reference renderer (sb/oracle.py; §8f row 3) -----------------
+
+@pytest.mark.parametrize("name", ["g_sh3_baseline", "g_sh0_aabb"])
+def test_render_reference_matches_golden(name):
+    """The reference asserts render_reference == run_pipeline bitwise
+    (sb tests/test_oracle.py:58-65); the goldens hold the pipeline's image."""
+    from conftest import bits_equal, golden_arrays, golden_camera, load_golden
+
+    import paper_2409_08669_b200 as ab
+
+    g = load_golden(name)
+    ds = ab.DeviceScene.from_arrays(golden_arrays(g), int(g["sh_degree"]), "cuda")
+    img, lm = ab.render_reference(ds, golden_camera(g))
+    assert bits_equal(img.pixels.cpu().numpy(), g["pixels"])
+    assert np.array_equal(lm.counts.cpu().numpy(), g["load"])
+
+
+def test_render_reference_equals_pipeline_fullsize():
+    """Large-N self-check with no CPU oracle: the garden-scale frame
+    (5.8M Gaussians, 48.8M pairs) through the binning-free path equals the
+    fused pipeline bit for bit."""
+    import sys
+
+    import torch
+
+    from conftest import ROOT
+    if str(ROOT) not in sys.path:
+        sys.path.insert(0, str(ROOT))
+    import bench
+    import paper_2409_08669_b200 as ab
+
+    cfg = bench.CONFIGS["garden"]
+    a = bench.scene_arrays(cfg)
+    cam = bench.cameras(cfg, 8)[1]
+    ds = ab.DeviceScene.from_arrays(a, cfg["sh"], "cuda", torch.float32)
+    res = ab.run_pipeline(ds, cam, mode="aabb")
+    img, lm = ab.render_reference(ds, cam)
+    assert torch.equal(img.pixels.view(torch.int32), res.image.pixels.view(torch.int32))
+    assert torch.equal(lm.counts, res.load_map.counts)
