@@ -8,6 +8,10 @@ exceptions, backed by hand-written sm_100a kernels in libadrsplat.so
 """
 
 from .errors import CapacityError, InternalError, SceneFormatError, SceneValidationError
+from .footprint import (CullExtent, EllipseCoefficients, ProjectedGaussian, aabb_extents,
+                        bounding_box_halfwidths, bounding_circle_radius, build_covariance3d,
+                        composite_pixels, eigen_extents, ellipse_coefficients, evaluate_sh,
+                        project_gaussian, quaternion_to_rotation, radius_adaptive, radius_baseline)
 from .metrics import (DEFAULT_WEIGHTS, PSNR_IDENTICAL_SENTINEL, BalanceStepResult, LoadStats,
                       LossWeights, l1_loss, load_loss, psnr, replace_opacity, ssim, toy_balance_step,
                       total_loss)
@@ -36,7 +40,10 @@ __all__ = [
     "TilePairList", "TileRect", "build_pairs", "SceneDiagnostic", "load_json", "load_ply",
     "load_ply_arrays", "load_scene", "load_scene_arrays", "normalize_quaternion", "save_json",
     "save_ply", "save_scene", "validate_scene", "DEFAULT_WEIGHTS", "BalanceStepResult", "LossWeights",
-    "l1_loss", "render_reference", "replace_opacity", "ssim", "toy_balance_step", "total_loss", "duplicate_with_keys", "generate_synthetic",
+    "l1_loss", "render_reference", "CullExtent", "EllipseCoefficients", "ProjectedGaussian",
+    "aabb_extents", "bounding_box_halfwidths", "bounding_circle_radius", "build_covariance3d",
+    "composite_pixels", "eigen_extents", "ellipse_coefficients", "evaluate_sh", "project_gaussian",
+    "quaternion_to_rotation", "radius_adaptive", "radius_baseline", "replace_opacity", "ssim", "toy_balance_step", "total_loss", "duplicate_with_keys", "generate_synthetic",
     "identify_tile_ranges", "inclusive_sum", "load_loss", "preprocess", "psnr", "render",
     "run_pipeline", "sort_pairs", "synthetic_arrays", "tiles_touched", "touched_counts",
 ]
