@@ -51,17 +51,16 @@ struct ProjSource {
     }
 };
 
-// Rows 4w .. 4w+3 of the tile belong to warp w: bit w of the mask is set when
-// the splat's conservative box (mx +- hx, my +- hy) meets those pixel rows
-// and the tile's pixel columns.
+// Warp w owns the 8x8 quadrant (qx, qy) = (w & 1, w >> 1) of the tile (a
+// square footprint meets fewer small splats than a 4x16 strip): bit w of the
+// mask is set when the splat's conservative box (mx +- hx, my +- hy) meets the
+// quadrant's pixel columns and rows.
 __device__ __forceinline__ uint32_t warp_mask(const Record& r, float x_lo, float y_lo) {
     const float mx = r.a.x, my = r.a.y, hx = r.c.z, hy = r.c.w;
-    if (!(mx - hx <= x_lo + (kTile - 1)) || !(mx + hx >= x_lo)) return 0u;
-    const float lo = fmaxf(fminf(ceilf(0.25f * ((my - hy) - y_lo - 3.0f)), 4.0f), 0.0f);
-    const float hi = fmaxf(fminf(floorf(0.25f * ((my + hy) - y_lo)), 3.0f), -1.0f);
-    const int w0 = (int)lo, w1 = (int)hi;
-    if (w1 < w0) return 0u;
-    return ((2u << w1) - 1u) & ~((1u << w0) - 1u);
+    const float l = mx - hx, rr = mx + hx, t = my - hy, b = my + hy;
+    const uint32_t xm = (uint32_t)(l <= x_lo + 7.0f && rr >= x_lo) | ((uint32_t)(l <= x_lo + 15.0f && rr >= x_lo + 8.0f) << 1);
+    const uint32_t ym = (uint32_t)(t <= y_lo + 7.0f && b >= y_lo) | ((uint32_t)(t <= y_lo + 15.0f && b >= y_lo + 8.0f) << 1);
+    return (xm * ((ym & 1u) | ((ym & 2u) << 1)));  // bits: (qy,qx) = 0:(0,0) 1:(0,1) 2:(1,0) 3:(1,1)
 }
 
 // One pixel's blend step with the full exp_np (slow splats).
@@ -103,8 +102,8 @@ k_render(Src src, const int64_t* __restrict__ ranges, int32_t width, int32_t hei
     const int tile = order ? (int)order[blockIdx.x] : (int)blockIdx.x;
     const int ty = tile / tiles_x, tx = tile - ty * tiles_x;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const int px0 = tx * kTile + 2 * (lane & 7);
-    const int py = ty * kTile + 4 * warp + (lane >> 3);
+    const int px0 = tx * kTile + 8 * (warp & 1) + 2 * (lane & 3);
+    const int py = ty * kTile + 8 * (warp >> 1) + (lane >> 2);
     const bool in0 = px0 < width && py < height, in1 = px0 + 1 < width && py < height;
     const int64_t start = ranges[2 * tile], end = ranges[2 * tile + 1];
     const float fpx0 = (float)px0, fpx1 = (float)(px0 + 1), fpy = (float)py;
