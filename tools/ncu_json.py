@@ -1,0 +1,50 @@
+"""profiles/ncu_summary.json from an ncu launch list (+ optional full report):
+per-config DRAM bytes per launch of k_render / k_preprocess and the render's
+FMA-pipe activity, read by bench.py for the roofline `traffic` fields.
+
+    python tools/ncu_json.py garden gpurun_out/launches_X.csv [gpurun_out/full.ncu-rep]
+"""
+import csv
+import io
+import json
+import subprocess
+import sys
+from pathlib import Path
+
+OUT = Path(__file__).resolve().parents[1] / "profiles" / "ncu_summary.json"
+SCALE = {"byte": 1.0, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}
+
+
+def launches(path):
+    rows = list(csv.reader(open(path)))
+    h = next(i for i, r in enumerate(rows) if "Kernel Name" in r)
+    hdr, data = rows[h], rows[h + 1:]
+    ki, mi, vi, ui = (hdr.index(x) for x in ("Kernel Name", "Metric Name", "Metric Value", "Metric Unit"))
+    out = {}
+    for r in data:
+        name = "k_render" if "k_render<" in r[ki] else ("k_preprocess" if "k_preprocess<" in r[ki] else None)
+        if name and r[mi].startswith("dram__bytes"):
+            out[name] = out.get(name, 0.0) + float(r[vi].replace(",", "")) * SCALE.get(r[ui], 1.0)
+    return out
+
+
+def main(config, csv_path, rep=None):
+    d = json.loads(OUT.read_text()) if OUT.exists() else {}
+    b = launches(csv_path)
+    e = d.setdefault(config, {})
+    e["k_render_dram_bytes"] = b.get("k_render")
+    e["k_preprocess_dram_bytes"] = b.get("k_preprocess")
+    e["source"] = str(csv_path)
+    if rep:
+        txt = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv", "--kernel-name", "regex:k_render",
+                              "--metrics", "sm__pipe_fma_cycles_active.avg.pct_of_peak_sustained_active"],
+                             capture_output=True, text=True).stdout
+        rows = list(csv.reader(io.StringIO(txt)))
+        i = rows[0].index("sm__pipe_fma_cycles_active.avg.pct_of_peak_sustained_active")
+        e["k_render_fma_pipe"] = float(rows[2][i]) / 100.0
+    OUT.write_text(json.dumps(d, indent=1) + "\n")
+    print(json.dumps(d, indent=1))
+
+
+if __name__ == "__main__":
+    main(*sys.argv[1:])
