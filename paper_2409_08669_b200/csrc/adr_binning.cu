@@ -332,27 +332,39 @@ k_emit_stage(const uint4* __restrict__ rinfo, const uint32_t* __restrict__ off, 
 }
 
 // ranges[t] = (lower_bound(t), lower_bound(t+1)) over sorted tile ids; each
-// thread owns 8 consecutive positions (one 16-byte load for u16 ids) and
-// writes the boundaries that fall on them; position p (the end) is owned by
-// the thread whose range contains it.
+// thread owns 16 consecutive positions (two 16-byte loads for u16 ids; the
+// element before them comes from the neighbouring lane) and writes the
+// boundaries that fall on them; position p (the end) is owned by the thread
+// whose range contains it.  Sorted input: a chunk whose first and last ids
+// equal its predecessor's holds no boundary (the common case) and exits.
 template <typename TileT>
 __global__ void k_ranges_tiles(const TileT* __restrict__ tiles, const int64_t* __restrict__ d_p, int64_t n_tiles,
                                int64_t* __restrict__ ranges) {
+    constexpr int kPer = 16;
     const int64_t p = *d_p;
-    const int64_t i0 = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) * 8;
-    if (i0 > p) return;
-    TileT v[9];
-    v[0] = i0 == 0 ? TileT(0) : tiles[i0 - 1];
-    if (sizeof(TileT) == 2 && i0 + 8 <= p) {
-        const uint4 q = *reinterpret_cast<const uint4*>(tiles + i0);
+    const int64_t i0 = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) * kPer;
+    TileT v[kPer + 1];
+    const bool full = sizeof(TileT) == 2 && i0 + kPer <= p;
+    if (full) {
+        const uint4 q0 = *reinterpret_cast<const uint4*>(tiles + i0);
+        const uint4 q1 = *reinterpret_cast<const uint4*>(tiles + i0 + 8);
 #pragma unroll
-        for (int k = 0; k < 8; ++k) v[k + 1] = reinterpret_cast<const TileT*>(&q)[k];
+        for (int k = 0; k < 8; ++k) {
+            v[k + 1] = reinterpret_cast<const TileT*>(&q0)[k];
+            v[k + 9] = reinterpret_cast<const TileT*>(&q1)[k];
+        }
     } else {
 #pragma unroll
-        for (int k = 0; k < 8; ++k) v[k + 1] = i0 + k < p ? tiles[i0 + k] : TileT(0);
+        for (int k = 0; k < kPer; ++k) v[k + 1] = i0 + k < p ? tiles[i0 + k] : TileT(0);
     }
+    // predecessor: last id of the lane to the left (lane 0 loads it)
+    const int lane = threadIdx.x & 31;
+    const TileT left = (TileT)__shfl_up_sync(0xffffffffu, (uint32_t)v[kPer], 1);
+    v[0] = lane ? left : (i0 > 0 && i0 - 1 < p ? tiles[i0 - 1] : TileT(0));
+    if (i0 > p) return;
+    if (full && i0 > 0 && v[0] == v[kPer] && i0 + kPer < p) return;
 #pragma unroll
-    for (int k = 0; k < 8; ++k) {
+    for (int k = 0; k < kPer; ++k) {
         const int64_t i = i0 + k;
         if (i > p) break;
         const int64_t prev = i == 0 ? -1 : (int64_t)v[k];
@@ -437,7 +449,7 @@ static int32_t frame_binning_t(const FrameBinning& fb, cudaStream_t st) {
     if (rc) return rc;
     if (fb.ev_after_sort) ADR_CUDA_TRY(cudaEventRecord(fb.ev_after_sort, st));
     // (f) tile ranges
-    k_ranges_tiles<TileT><<<ceil_div(ceil_div(cap + 1, 8), 256), 256, 0, st>>>(stiles, ctr + 3, fb.n_tiles, fb.ranges);
+    k_ranges_tiles<TileT><<<ceil_div(ceil_div(cap + 1, 16), 256), 256, 0, st>>>(stiles, ctr + 3, fb.n_tiles, fb.ranges);
     ADR_LAUNCH_CHECK();
     if (fb.ev_after_ranges) ADR_CUDA_TRY(cudaEventRecord(fb.ev_after_ranges, st));
     return ADR_OK;
