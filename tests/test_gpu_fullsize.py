@@ -112,3 +112,63 @@ def test_fullsize_graph_replay_deterministic():
     assert torch.equal(rast.pixels.view(torch.int32), img0.view(torch.int32))
     assert torch.equal(rast.load, load0)
     assert torch.equal(rast.keys[:p0], keys0)
+
+
+def test_view_renderer_matches_single_view_frames():
+    """Views in flight (several Rasterizers on their own streams) give every
+    view exactly its single-view run_pipeline output; the overflow path
+    (a slot too small for a view) re-renders and still matches."""
+    import torch
+
+    import paper_2409_08669_b200 as ab
+    from paper_2409_08669_b200.views import ViewRenderer, orbit_cameras
+
+    a = ab.synthetic_arrays(12, 60000, ab.SyntheticSpec(extent=1.0, scale_range=(0.004, 0.03),
+                                                        anisotropy_range=(1, 5), opacity_range=(0.01, 0.9)),
+                            sh_degree=1, float32=True)
+    ds = ab.DeviceScene.from_arrays(a, 1, "cuda", torch.float32)
+    cams = orbit_cameras(7, 320, 200, radius=2.6, background=(0.1, 0.2, 0.3))
+    vr = ViewRenderer(ds, 320, 200, in_flight=3)
+    for s in vr.slots[1:]:
+        s.cap = 0
+        s._ensure_capacity(50_000)   # forces the overflow/re-render path for some views
+    px, ld, st = vr.render(cams)
+    for i, cam in enumerate(cams):
+        res = ab.run_pipeline(ds, cam, mode="aabb")
+        assert torch.equal(px[i].view(torch.int32), res.image.pixels.view(torch.int32)), i
+        assert torch.equal(ld[i], res.load_map.counts), i
+        ls = res.load_stats
+        assert st[i].tolist() == [res.stats.pair_count, res.stats.culled_gaussians,
+                                  int(res.load_map.counts.long().sum()), int((res.load_map.counts.long() ** 2).sum()),
+                                  ls.min, ls.max]
+
+
+def test_render_views_sharded_single_rank_nccl():
+    """The multi-GPU entry point on a one-rank NCCL group (the only GPU
+    count this run has): shard -> render -> all_gather -> view order."""
+    import os
+    import socket
+
+    import torch
+    import torch.distributed as dist
+
+    import paper_2409_08669_b200 as ab
+    from paper_2409_08669_b200.views import orbit_cameras, render_views_sharded
+
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        port = s.getsockname()[1]
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("nccl", rank=0, world_size=1, device_id=torch.device("cuda", 0))
+    try:
+        a = ab.synthetic_arrays(13, 20000, ab.SyntheticSpec(), sh_degree=0, float32=True)
+        ds = ab.DeviceScene.from_arrays(a, 0, "cuda", torch.float32)
+        cams = orbit_cameras(5, 128, 96, radius=5.0)
+        px, ld, st = render_views_sharded(ds, cams, in_flight=2)
+        for i, cam in enumerate(cams):
+            res = ab.run_pipeline(ds, cam)
+            assert torch.equal(px[i].view(torch.int32), res.image.pixels.view(torch.int32))
+            assert torch.equal(ld[i], res.load_map.counts)
+            assert int(st[i, 0]) == res.stats.pair_count
+    finally:
+        dist.destroy_process_group()
