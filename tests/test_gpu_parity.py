@@ -392,3 +392,59 @@ def test_capacity_regrow():
     assert rast.cap >= res.stats.pair_count > 1000
     assert np.array_equal(_np(res.pairs.keys), _np(ref.pairs.keys))
     assert bits_equal(_np(res.image.pixels), _np(ref.image.pixels))
+
+
+def _oracle_check(oracle, arrays, deg, cam, mode):
+    import torch
+
+    import paper_2409_08669_b200 as ab
+
+    ds = ab.DeviceScene.from_arrays(arrays, deg, "cuda", torch.float64)
+    res = ab.run_pipeline(ds, cam, mode=mode)
+    ref = oracle.run_pipeline(dict(centers=arrays.centers, scales=arrays.scales, rotations=arrays.rotations,
+                                   opacities=arrays.opacities, sh=arrays.sh, sh_degree=deg), cam, mode)
+    p = res.pairs.to_numpy()
+    assert res.stats.pair_count == len(ref["keys"])
+    assert np.array_equal(p["keys"], ref["keys"])
+    assert np.array_equal(p["gaussian_indices"], ref["gidx"])
+    assert np.array_equal(p["tile_ranges"], ref["ranges"])
+    assert bits_equal(_np(res.image.pixels), ref["pixels"])
+    assert np.array_equal(_np(res.load_map.counts), ref["load"])
+    return res
+
+
+@pytest.mark.parametrize("w,h", [(1, 1), (17, 5), (15, 33), (16, 16), (255, 1)])
+def test_edge_image_sizes_vs_oracle(oracle, w, h):
+    import paper_2409_08669_b200 as ab
+
+    a = ab.synthetic_arrays(71, 3000, mixed_spec(), sh_degree=2)
+    cam = ab.Camera.from_lookat((0.0, 0.0, -4.0), (0, 0, 0), width=w, height=h, background=(0.3, 0.1, 0.2))
+    for mode in ("baseline", "aabb"):
+        _oracle_check(oracle, a, 2, cam, mode)
+
+
+def test_edge_scenes_vs_oracle(oracle):
+    """All behind the camera (P = 0); a giant splat covering every tile next
+    to ordinary ones; many splats at one identical depth (tie-break by index,
+    SURVEY H3); opacity exactly 1; splats straddling the near plane."""
+    import paper_2409_08669_b200 as ab
+
+    cam = ab.Camera.from_lookat((0.0, 0.0, -3.0), (0, 0, 0), width=96, height=80, background=(0.1, 0.2, 0.3))
+    base = ab.synthetic_arrays(72, 600, mixed_spec(), sh_degree=1)
+    behind = base._replace(centers=base.centers + np.array([0.0, 0.0, -10.0]))
+    r = _oracle_check(oracle, behind, 1, cam, "aabb")
+    assert r.stats.pair_count == 0 and r.stats.culled_gaussians == 600
+    giant = base._replace(scales=base.scales.copy())
+    giant.scales[7] = (3.0, 3.0, 3.0)
+    giant.opacities[7] = 0.8
+    _oracle_check(oracle, giant, 1, cam, "baseline")
+    _oracle_check(oracle, giant, 1, cam, "aabb")
+    ties = base._replace(centers=base.centers.copy(), opacities=base.opacities.copy())
+    ties.centers[:, 2] = 0.25              # one depth for everybody
+    ties.opacities[::5] = 1.0
+    r = _oracle_check(oracle, ties, 1, cam, "circle")
+    k = r.pairs.to_numpy()["keys"]
+    assert (k[1:] == k[:-1]).sum() > 1000   # heavy key ties, resolved by Gaussian index
+    near = base._replace(centers=base.centers.copy())
+    near.centers[:, 2] = np.linspace(-2.9, -2.7, 600)   # around the 0.2 near plane
+    _oracle_check(oracle, near, 1, cam, "aabb")
