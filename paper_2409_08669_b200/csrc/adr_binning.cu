@@ -274,60 +274,52 @@ struct RankOffsetsOp {
 // np.argsort(keys, kind="stable") (tiling.py:159-164) because ranks are
 // ordered by (depth bits, Gaussian index).
 
-constexpr int kEmitWarps = 8;
-constexpr int kEmitStage = 1024;   // staged positions per warp and piece
-
-// Emission of the rank-ordered stream as (tile id, Gaussian index).  A warp
-// owns 32 consecutive ranks, i.e. the contiguous stream range
-// [off[r0], off[r0+32]); each lane expands its own rectangle row-major into a
-// per-warp shared-memory staging buffer, and the warp then copies the staged
-// piece out with coalesced stores.
+// Balanced emission: a warp owns 32 consecutive ranks and the contiguous
+// stream range [off[r0], off[r0 + 32]); lane l writes positions
+// wstart + l, wstart + l + 32, ... (coalesced stores), finding each position's
+// owner among the warp's ranks with a 5-step shuffle search over the lanes'
+// start offsets, so lanes do equal work however uneven the rectangles are.
 template <typename TileT>
-__global__ void __launch_bounds__(kEmitWarps * 32)
-k_emit_stage(const uint4* __restrict__ rinfo, const uint32_t* __restrict__ off, const int64_t* __restrict__ d_m,
-             const int64_t* __restrict__ d_pc, int32_t tiles_x, TileT* __restrict__ tiles, uint32_t* __restrict__ gs) {
-    extern __shared__ __align__(16) unsigned char emit_smem[];
-    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    TileT* st_t = reinterpret_cast<TileT*>(emit_smem) + warp * kEmitStage;
-    uint32_t* st_g = reinterpret_cast<uint32_t*>(emit_smem + sizeof(TileT) * kEmitWarps * kEmitStage) + warp * kEmitStage;
+__global__ void __launch_bounds__(256)
+k_emit_balanced(const uint4* __restrict__ rinfo, const uint32_t* __restrict__ off, const int64_t* __restrict__ d_m,
+                const int64_t* __restrict__ d_pc, int32_t tiles_x, TileT* __restrict__ tiles, uint32_t* __restrict__ gs) {
+    const int lane = threadIdx.x & 31;
     const uint32_t m = (uint32_t)*d_m;
     const uint32_t pc = (uint32_t)*d_pc;
-    const uint32_t r0 = (blockIdx.x * kEmitWarps + warp) * 32u;
+    const uint32_t r0 = (uint32_t)(((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5) * 32u;
     if (r0 >= m) return;
     const uint32_t r = r0 + lane;
     const bool valid = r < m;
     const uint4 inf = valid ? rinfo[r] : make_uint4(0, 0, 0, 0);
-    const uint32_t x0 = inf.x & 0xffffu, x1 = inf.x >> 16, y0 = inf.y & 0xffffu, y1 = inf.y >> 16;
-    const uint32_t wdt = x1 - x0;
     const uint32_t o = valid ? off[r] : pc;
-    const uint32_t c = valid ? wdt * (y1 - y0) : 0u;
     const uint32_t wstart = __shfl_sync(kFull, o, 0);
     uint32_t wend = r0 + 32 < m ? off[r0 + 32] : pc;
     wend = wend < pc ? wend : pc;
-    const uint32_t oe = o + c;
-    for (uint32_t ps = wstart; ps < wend; ps += kEmitStage) {
-        const uint32_t pe = ps + kEmitStage < wend ? ps + kEmitStage : wend;
-        const uint32_t a = o > ps ? o : ps;
-        const uint32_t b = oe < pe ? oe : pe;
-        if (a < b) {
-            uint32_t j = a - o;
-            uint32_t ty = y0 + j / wdt;
-            uint32_t tx = x0 + (j - (ty - y0) * wdt);
-            for (uint32_t q = a - ps; q < b - ps; ++q) {
-                st_t[q] = (TileT)(ty * (uint32_t)tiles_x + tx);
-                st_g[q] = inf.z;
-                if (++tx == x1) {
-                    tx = x0;
-                    ++ty;
-                }
-            }
+    const uint32_t x0 = inf.x & 0xffffu, w = (inf.x >> 16) - x0, y0 = inf.y & 0xffffu;
+    const float rw = w ? __frcp_rn((float)w) : 0.0f;
+    for (uint32_t base = wstart; base < wend; base += 32) {
+        const uint32_t q = base + lane;
+        // owner: the last lane whose start offset is <= q
+        int L = 0;
+#pragma unroll
+        for (int step = 16; step > 0; step >>= 1) {
+            const uint32_t oc = __shfl_sync(kFull, o, L + step);
+            if (L + step < 32 && oc <= q) L += step;
         }
-        __syncwarp();
-        for (uint32_t q = lane; q < pe - ps; q += 32) {
-            tiles[ps + q] = st_t[q];
-            gs[ps + q] = st_g[q];
+        const uint32_t oL = __shfl_sync(kFull, o, L);
+        const uint32_t wL = __shfl_sync(kFull, w, L);
+        const float rwL = __shfl_sync(kFull, rw, L);
+        const uint32_t xL = __shfl_sync(kFull, x0, L), yL = __shfl_sync(kFull, y0, L);
+        const uint32_t gL = __shfl_sync(kFull, inf.z, L);
+        if (q < wend) {
+            const uint32_t j = q - oL;
+            uint32_t row = (uint32_t)((float)j * rwL);
+            int32_t col = (int32_t)j - (int32_t)(row * wL);
+            if (col < 0) { --row; col += (int32_t)wL; }
+            if (col >= (int32_t)wL) { ++row; col -= (int32_t)wL; }
+            tiles[q] = (TileT)((yL + row) * (uint32_t)tiles_x + xL + (uint32_t)col);
+            gs[q] = gL;
         }
-        __syncwarp();
     }
 }
 
@@ -429,13 +421,8 @@ static int32_t frame_binning_t(const FrameBinning& fb, cudaStream_t st) {
     int tbits = 0;
     while ((int64_t(1) << tbits) < fb.n_tiles) ++tbits;
     if (tbits == 0) tbits = 1;
-    {
-        const size_t esm = (sizeof(TileT) + sizeof(uint32_t)) * kEmitWarps * kEmitStage;
-        ADR_CUDA_TRY(cudaFuncSetAttribute(k_emit_stage<TileT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)esm));
-        k_emit_stage<TileT><<<ceil_div(n, kEmitWarps * 32), kEmitWarps * 32, esm, st>>>(rinfo, off, ctr + 2, ctr + 3,
-                                                                                        fb.tiles_x, tiles, gs);
-        ADR_LAUNCH_CHECK();
-    }
+    k_emit_balanced<TileT><<<ceil_div(n, 256), 256, 0, st>>>(rinfo, off, ctr + 2, ctr + 3, fb.tiles_x, tiles, gs);
+    ADR_LAUNCH_CHECK();
     if (fb.ev_after_dup) ADR_CUDA_TRY(cudaEventRecord(fb.ev_after_dup, st));
     // (e) stable radix sort by tile id; the last pass writes the sorted
     //     Gaussian indices (the render's record index and the gidx export)
