@@ -416,8 +416,15 @@ def run_ours(args, cfg, rank, world, local):
     if dist and world > 1:
         from paper_2409_08669_b200.views import STATS_FIELDS, gather_frames, pack_frame
 
-        frames = torch.stack([pack_frame(rast.pixels, rast.load)] * len(mine))
+        # this rank's real frames and stats, one replay per view
+        frames = torch.empty((len(mine), cfg["h"], cfg["w"], 4), dtype=torch.float32, device=dev)
         st = torch.zeros((len(mine), len(STATS_FIELDS)), dtype=torch.int64, device=dev)
+        for v, g in enumerate(graphs):
+            r = rasts[v % n_fly]
+            g.replay()
+            frames[v].copy_(pack_frame(r.pixels, r.load))
+            st[v, 0:2].copy_(r.counters[0:2])
+            st[v, 2:4].copy_(r.stats[0:2])
         torch.cuda.synchronize(dev)
         g0 = time.perf_counter()
         gather_frames(frames, st, n_views)
