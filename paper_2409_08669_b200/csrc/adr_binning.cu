@@ -297,19 +297,20 @@ k_emit_balanced(const uint4* __restrict__ rinfo, const uint32_t* __restrict__ of
     wend = wend < pc ? wend : pc;
     const uint32_t x0 = inf.x & 0xffffu, w = (inf.x >> 16) - x0, y0 = inf.y & 0xffffu;
     const float rw = w ? __frcp_rn((float)w) : 0.0f;
+    const uint32_t xy0 = x0 | (y0 << 16);
     for (uint32_t base = wstart; base < wend; base += 32) {
         const uint32_t q = base + lane;
-        // owner: the last lane whose start offset is <= q
-        int L = 0;
-#pragma unroll
-        for (int step = 16; step > 0; step >>= 1) {
-            const uint32_t oc = __shfl_sync(kFull, o, L + step);
-            if (L + step < 32 && oc <= q) L += step;
-        }
+        // owner of position q: (ranks starting at or before q) - 1, from a
+        // ballot of the ranks that start before this window and the OR of
+        // the in-window start bits (starts are distinct: every rank owns >= 1)
+        const uint32_t before = __popc(__ballot_sync(kFull, valid && o < base));
+        const uint32_t d = o - base;
+        const uint32_t starts = __reduce_or_sync(kFull, (valid && o >= base && d < 32u) ? (1u << d) : 0u);
+        const int L = (int)(before + __popc(starts & ((2u << lane) - 1u))) - 1;
         const uint32_t oL = __shfl_sync(kFull, o, L);
         const uint32_t wL = __shfl_sync(kFull, w, L);
         const float rwL = __shfl_sync(kFull, rw, L);
-        const uint32_t xL = __shfl_sync(kFull, x0, L), yL = __shfl_sync(kFull, y0, L);
+        const uint32_t xyL = __shfl_sync(kFull, xy0, L);
         const uint32_t gL = __shfl_sync(kFull, inf.z, L);
         if (q < wend) {
             const uint32_t j = q - oL;
@@ -317,7 +318,7 @@ k_emit_balanced(const uint4* __restrict__ rinfo, const uint32_t* __restrict__ of
             int32_t col = (int32_t)j - (int32_t)(row * wL);
             if (col < 0) { --row; col += (int32_t)wL; }
             if (col >= (int32_t)wL) { ++row; col -= (int32_t)wL; }
-            tiles[q] = (TileT)((yL + row) * (uint32_t)tiles_x + xL + (uint32_t)col);
+            tiles[q] = (TileT)(((xyL >> 16) + row) * (uint32_t)tiles_x + (xyL & 0xffffu) + (uint32_t)col);
             gs[q] = gL;
         }
     }
