@@ -105,6 +105,18 @@ k_preprocess(const T* __restrict__ centers, const T* __restrict__ scales,
     T* stage = reinterpret_cast<T*>(pre_smem);
     const int64_t first = (int64_t)blockIdx.x * kPreBlock;
     const int64_t i = first + threadIdx.x;
+    // per-Gaussian attributes first, so their latency overlaps the SH staging
+    T ac[3] = {T(0), T(0), T(0)}, as[3] = {T(0), T(0), T(0)}, aq[4] = {T(0), T(0), T(0), T(0)}, aop = T(0);
+    if (i < n) {
+#pragma unroll
+        for (int k = 0; k < 3; ++k) {
+            ac[k] = centers[3 * i + k];
+            as[k] = scales[3 * i + k];
+        }
+#pragma unroll
+        for (int k = 0; k < 4; ++k) aq[k] = rotations[4 * i + k];
+        aop = opacities[i];
+    }
     stage_sh<T, DEG>(sh, first, (int)(n - first < kPreBlock ? n - first : kPreBlock), stage);
     __syncthreads();
     bool alive = false;
@@ -112,8 +124,7 @@ k_preprocess(const T* __restrict__ centers, const T* __restrict__ scales,
     uint32_t dbits = 0;      // fused: float32 depth bits
     if (i < n) {
         const double* R = cam.rot;
-        const double c0 = (double)centers[3 * i], c1 = (double)centers[3 * i + 1],
-                     c2 = (double)centers[3 * i + 2];
+        const double c0 = (double)ac[0], c1 = (double)ac[1], c2 = (double)ac[2];
         double pv[3];
 #pragma unroll
         for (int k = 0; k < 3; ++k)
@@ -121,8 +132,7 @@ k_preprocess(const T* __restrict__ centers, const T* __restrict__ scales,
         const double depth = pv[2];
         alive = depth > cam.near_plane;
 
-        const double w = (double)rotations[4 * i], x = (double)rotations[4 * i + 1],
-                     y = (double)rotations[4 * i + 2], z = (double)rotations[4 * i + 3];
+        const double w = (double)aq[0], x = (double)aq[1], y = (double)aq[2], z = (double)aq[3];
         double rq[9];
         rq[0] = SUB(1.0, MUL(2.0, ADD(MUL(y, y), MUL(z, z))));
         rq[1] = MUL(2.0, SUB(MUL(x, y), MUL(w, z)));
@@ -133,7 +143,7 @@ k_preprocess(const T* __restrict__ centers, const T* __restrict__ scales,
         rq[6] = MUL(2.0, SUB(MUL(x, z), MUL(w, y)));
         rq[7] = MUL(2.0, ADD(MUL(y, z), MUL(w, x)));
         rq[8] = SUB(1.0, MUL(2.0, ADD(MUL(x, x), MUL(y, y))));
-        const double s0 = (double)scales[3 * i], s1 = (double)scales[3 * i + 1], s2 = (double)scales[3 * i + 2];
+        const double s0 = (double)as[0], s1 = (double)as[1], s2 = (double)as[2];
         double m[9];
 #pragma unroll
         for (int a = 0; a < 3; ++a) {
@@ -179,7 +189,7 @@ k_preprocess(const T* __restrict__ centers, const T* __restrict__ scales,
         const double mx = ADD(MUL(MUL(cam.fx, pv[0]), inv_z), cam.cx);
         const double my = ADD(MUL(MUL(cam.fy, pv[1]), inv_z), cam.cy);
         const double r_o_real = MUL(3.0, __dsqrt_rn(np_max(lam_max, 0.0)));
-        const double sigma = (double)opacities[i];
+        const double sigma = (double)aop;
         double ex, ey;
         if (mode == ADR_MODE_BASELINE) {
             ex = ceil(r_o_real);
