@@ -17,7 +17,8 @@ import numpy as np
 from .errors import CapacityError, InternalError
 
 _PKG = Path(__file__).resolve().parent
-LIB_PATH = _PKG / "_build" / "libadrsplat.so"
+# ADR_LIBRARY overrides the in-tree build (used to A/B kernel variants: tools/variants.sh)
+LIB_PATH = Path(os.environ.get("ADR_LIBRARY", _PKG / "_build" / "libadrsplat.so"))
 CSRC = _PKG / "csrc"
 HEADER = _PKG.parent / "include" / "adr_splat.h"
 

@@ -86,8 +86,12 @@ __device__ __forceinline__ void blend_scalar(float fpx, float fpy, const float4&
     if (T < term) done = true;
 }
 
-template <class Src>
-__global__ void __launch_bounds__(kRenderThreads)
+// kFlagDone: a pixel's "done" state is an explicit flag.  When the
+// termination threshold is <= 1 it is implied by T itself (T starts at 1, only
+// contributing blends change it and the reference tests T < term right after
+// each of them, render.py:110-112), so the flags — and their registers — go.
+template <class Src, bool kFlagDone>
+__global__ void __launch_bounds__(kRenderThreads, 8)
 k_render(Src src, const int64_t* __restrict__ ranges, int32_t width, int32_t height, int32_t tiles_x, float bg0,
          float bg1, float bg2, float alpha_low, float term, float* __restrict__ pixels, int32_t* __restrict__ load,
          adr_load_stats* stats, int32_t* hist, int32_t hist_bins, F2K K, const uint32_t* __restrict__ order) {
@@ -110,11 +114,15 @@ k_render(Src src, const int64_t* __restrict__ ranges, int32_t width, int32_t hei
     const f2 PX = pk(fpx0, fpx1);
     const float x_lo = (float)(tx * kTile), y_lo = (float)(ty * kTile);
 
-    f2 T = K.one, C0 = 0ull, C1 = 0ull, C2 = 0ull;  // (+0, +0)
+    // pixels outside the image start done (T = 0 in the implied mode: they
+    // are never written)
+    f2 T = kFlagDone ? K.one : pk(in0 ? 1.0f : 0.0f, in1 ? 1.0f : 0.0f), C0 = 0ull, C1 = 0ull, C2 = 0ull;
     int cnt0 = 0, cnt1 = 0;
-    bool done0 = !in0, done1 = !in1;
+    bool fdone0 = !in0, fdone1 = !in1;
+#define DONE0 (kFlagDone ? fdone0 : lo_of(T) < term)
+#define DONE1 (kFlagDone ? fdone1 : hi_of(T) < term)
     for (int64_t b = start; b < end; b += kBatch) {
-        if (__syncthreads_count(done0 && done1) == kRenderThreads) break;
+        if (__syncthreads_count(DONE0 && DONE1) == kRenderThreads) break;
         const int nb = (int)((end - b) < kBatch ? (end - b) : kBatch);
         for (int i = threadIdx.x; i < nb; i += kRenderThreads) {
             const Record r = src.load(b + i);
@@ -124,13 +132,12 @@ k_render(Src src, const int64_t* __restrict__ ranges, int32_t width, int32_t hei
             smask[i] = (uint8_t)warp_mask(r, x_lo, y_lo);
         }
         __syncthreads();
-        if (__any_sync(kFull, !(done0 && done1))) {
+        if (__any_sync(kFull, !(DONE0 && DONE1))) {
             for (int c0 = 0; c0 < nb; c0 += 32) {
                 uint32_t m = __ballot_sync(kFull, c0 + lane < nb && ((smask[c0 + lane] >> warp) & 1u));
                 while (m) {
                     const int j = c0 + __ffs(m) - 1;
                     m &= m - 1u;
-                    if (done0 && done1) continue;
                     const float4 G = sG[j];
                     const float2 Tc = sT[j];
                     const float tau = Tc.y;
@@ -139,8 +146,11 @@ k_render(Src src, const int64_t* __restrict__ ranges, int32_t width, int32_t hei
                         float t0 = lo_of(T), t1 = hi_of(T);
                         float a0 = lo_of(C0), a1 = hi_of(C0), b0 = lo_of(C1), b1 = hi_of(C1);
                         float d0 = lo_of(C2), d1 = hi_of(C2);
-                        blend_scalar(fpx0, fpy, G, Tc, W, alpha_low, term, t0, a0, b0, d0, cnt0, done0);
-                        blend_scalar(fpx1, fpy, G, Tc, W, alpha_low, term, t1, a1, b1, d1, cnt1, done1);
+                        bool d0f = DONE0, d1f = DONE1;
+                        blend_scalar(fpx0, fpy, G, Tc, W, alpha_low, term, t0, a0, b0, d0, cnt0, d0f);
+                        blend_scalar(fpx1, fpy, G, Tc, W, alpha_low, term, t1, a1, b1, d1, cnt1, d1f);
+                        fdone0 = d0f;
+                        fdone1 = d1f;
                         T = pk(t0, t1);
                         C0 = pk(a0, a1);
                         C1 = pk(b0, b1);
@@ -154,8 +164,8 @@ k_render(Src src, const int64_t* __restrict__ ranges, int32_t width, int32_t hei
                     const f2 q = add2(mul2(mul2(bc(G.z), dx, K), dx, K), bc(cdd), K);
                     const f2 bd = mul2(mul2(bc(G.w), dx, K), bc(dy), K);
                     const f2 pw = sub2(mul2(bc(-0.5f), q, K), bd, K);
-                    bool p0 = !done0 && lo_of(pw) >= tau;
-                    bool p1 = !done1 && hi_of(pw) >= tau;
+                    bool p0 = !DONE0 && lo_of(pw) >= tau;
+                    bool p1 = !DONE1 && hi_of(pw) >= tau;
                     if (!(p0 || p1)) continue;  // both alphas < alpha_low for sure
                     const float4 W = sW[j];
                     const f2 al = mul2(bc(W.x), exp2_np_fast(pw, K), K);
@@ -174,13 +184,17 @@ k_render(Src src, const int64_t* __restrict__ ranges, int32_t width, int32_t hei
                     T = mul2(T, sub2(K.one, A, K), K);
                     cnt0 += p0;
                     cnt1 += p1;
-                    if (p0 && lo_of(T) < term) done0 = true;
-                    if (p1 && hi_of(T) < term) done1 = true;
+                    if (kFlagDone) {
+                        if (p0 && lo_of(T) < term) fdone0 = true;
+                        if (p1 && hi_of(T) < term) fdone1 = true;
+                    }
                 }
-                if (__all_sync(kFull, done0 && done1)) break;
+                if (__all_sync(kFull, DONE0 && DONE1)) break;
             }
         }
     }
+#undef DONE0
+#undef DONE1
     const float t0 = lo_of(T), t1 = hi_of(T);
     const float o[2][3] = {{__fadd_rn(lo_of(C0), __fmul_rn(t0, bg0)), __fadd_rn(lo_of(C1), __fmul_rn(t0, bg1)),
                             __fadd_rn(lo_of(C2), __fmul_rn(t0, bg2))},
@@ -301,9 +315,10 @@ int32_t launch_render(const RenderArgs& a, cudaStream_t st) {
         k_tile_order<<<1, 1024, 0, st>>>(a.ranges, (int32_t)n_tiles, a.order);
         ADR_LAUNCH_CHECK();
     }
-    k_render<RecSource><<<n_tiles, kRenderThreads, 0, st>>>(src, a.ranges, a.width, a.height, a.tiles_x, a.bg[0], a.bg[1],
-                                                           a.bg[2], a.alpha_low, a.term, a.pixels, a.load, a.stats,
-                                                           a.hist, a.hist_bins, f2k_host(), a.order);
+    auto kern = a.term <= 1.0f ? k_render<RecSource, false> : k_render<RecSource, true>;
+    kern<<<n_tiles, kRenderThreads, 0, st>>>(src, a.ranges, a.width, a.height, a.tiles_x, a.bg[0], a.bg[1], a.bg[2],
+                                             a.alpha_low, a.term, a.pixels, a.load, a.stats, a.hist, a.hist_bins,
+                                             f2k_host(), a.order);
     ADR_LAUNCH_CHECK();
     return ADR_OK;
 }
@@ -315,8 +330,9 @@ int32_t launch_render_proj(const adr_projection& p, const int64_t* gidx, const i
     const int64_t n_tiles = (int64_t)tx * ty;
     if (n_tiles <= 0) return ADR_OK;
     ProjSource src{reinterpret_cast<const float2*>(p.d_mean2d), p.d_conic, p.d_opacity, p.d_color, gidx, alpha_low};
-    k_render<ProjSource><<<n_tiles, kRenderThreads, 0, st>>>(src, ranges, width, height, tx, bg[0], bg[1], bg[2],
-                                                            alpha_low, term, pixels, load, stats, hist, bins, f2k_host(), nullptr);
+    auto kern = term <= 1.0f ? k_render<ProjSource, false> : k_render<ProjSource, true>;
+    kern<<<n_tiles, kRenderThreads, 0, st>>>(src, ranges, width, height, tx, bg[0], bg[1], bg[2], alpha_low, term,
+                                             pixels, load, stats, hist, bins, f2k_host(), nullptr);
     ADR_LAUNCH_CHECK();
     return ADR_OK;
 }

@@ -251,6 +251,11 @@ class DeviceScene:
         """From a Scene (ours or the reference's, fp64) or a DeviceScene."""
         if isinstance(scene, DeviceScene):
             return scene.to(device)
+        if isinstance(scene, SceneArrays):   # degree from the (N, (d+1)^2, 3) SH block
+            deg = int(round(np.sqrt(scene.sh.shape[1]))) - 1
+            if (deg + 1) ** 2 != scene.sh.shape[1]:
+                raise ValueError(f"sh has {scene.sh.shape[1]} coefficients, not a square (d+1)^2")
+            return cls.from_arrays(scene, deg, device, dtype)
         return cls.from_arrays(scene.as_arrays(), int(scene.sh_degree), device, dtype)
 
     def to(self, device) -> "DeviceScene":

@@ -448,3 +448,27 @@ def test_edge_scenes_vs_oracle(oracle):
     near = base._replace(centers=base.centers.copy())
     near.centers[:, 2] = np.linspace(-2.9, -2.7, 600)   # around the 0.2 near plane
     _oracle_check(oracle, near, 1, cam, "aabb")
+
+
+@pytest.mark.parametrize("term", [1e-4, 0.3, 1.0, 1.5, 0.0, -1.0])
+def test_term_threshold_vs_oracle(oracle, term):
+    """Early-termination threshold (render.py:110-112) across the values that
+    select the render variants: term <= 1 (done implied by T < term) and
+    term > 1 (explicit done flags: the pixel stops after its first blend);
+    0 and negatives never terminate.  Frame API and stage API both."""
+    import paper_2409_08669_b200 as ab
+
+    a = ab.synthetic_arrays(73, 20000, mixed_spec(), sh_degree=1)
+    cam = ab.Camera.from_lookat((0.2, 0.1, -2.8), (0, 0, 0), width=150, height=110, background=(0.1, 0.3, 0.2))
+    res = ab.run_pipeline(a, cam, mode="aabb", term_threshold=term)
+    ref = oracle.run_pipeline(dict(centers=a.centers, scales=a.scales, rotations=a.rotations,
+                                   opacities=a.opacities, sh=a.sh, sh_degree=1), cam, "aabb",
+                              term_threshold=term)
+    assert bits_equal(_np(res.image.pixels), ref["pixels"])
+    assert np.array_equal(_np(res.load_map.counts), ref["load"])
+    grid = ab.TileGrid(cam.width, cam.height)
+    proj = ab.preprocess(a, cam, mode="aabb")
+    pairs = ab.build_pairs(proj, grid)
+    img, load = ab.render(proj, pairs, grid, cam, ab.ALPHA_LOW, term_threshold=term)
+    assert bits_equal(_np(img.pixels), ref["pixels"])
+    assert np.array_equal(_np(load.counts), ref["load"])
