@@ -23,6 +23,7 @@ constexpr int kBatch = 256;               // pairs staged per round
 
 // Record source for the fused frame: records by rank + per-pair rank list.
 struct RecSource {
+    static constexpr int kMinBlocks = 8;   // 64 registers
     const Record* rec;
     const uint32_t* idx;
     __device__ __forceinline__ Record load(int64_t j) const { return rec[idx[j]]; }
@@ -30,6 +31,7 @@ struct RecSource {
 
 // Record source for the stage API: Projection SoA + int64 Gaussian indices.
 struct ProjSource {
+    static constexpr int kMinBlocks = 6;   // the inline cull_params needs more registers
     const float2* mean2d;
     const float* conic;
     const float* opacity;
@@ -50,6 +52,25 @@ struct ProjSource {
         return r;
     }
 };
+
+// predicated increment (keeps the counter in place: no select + copy)
+__device__ __forceinline__ void inc_if(int& c, bool p) {
+    asm("{\n\t.reg .pred q;\n\tsetp.ne.b32 q, %1, 0;\n\t@q add.s32 %0, %0, 1;\n\t}" : "+r"(c) : "r"((int)p));
+}
+
+template <int kOff>
+__device__ __forceinline__ float4 lds_f4(uint32_t a) {
+    float4 v;
+    asm volatile("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4+%5];"
+                 : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w) : "r"(a), "n"(kOff));
+    return v;
+}
+template <int kOff>
+__device__ __forceinline__ float2 lds_f2(uint32_t a) {
+    float2 v;
+    asm volatile("ld.shared.v2.f32 {%0, %1}, [%2+%3];" : "=f"(v.x), "=f"(v.y) : "r"(a), "n"(kOff));
+    return v;
+}
 
 // Warp w owns the 8x8 quadrant (qx, qy) = (w & 1, w >> 1) of the tile (a
 // square footprint meets fewer small splats than a 4x16 strip): bit w of the
@@ -91,16 +112,20 @@ __device__ __forceinline__ void blend_scalar(float fpx, float fpy, const float4&
 // contributing blends change it and the reference tests T < term right after
 // each of them, render.py:110-112), so the flags — and their registers — go.
 template <class Src, bool kFlagDone>
-__global__ void __launch_bounds__(kRenderThreads, 8)
+__global__ void __launch_bounds__(kRenderThreads, Src::kMinBlocks)
 k_render(Src src, const int64_t* __restrict__ ranges, int32_t width, int32_t height, int32_t tiles_x, float bg0,
          float bg1, float bg2, float alpha_low, float term, float* __restrict__ pixels, int32_t* __restrict__ load,
          adr_load_stats* stats, int32_t* hist, int32_t hist_bins, F2K K, const uint32_t* __restrict__ order) {
     // shared-memory batch, split by use: the power test needs (mx, my, a, b)
     // + (c, tau); only splats that pass it read (sigma, r, g, b)
-    __shared__ float4 sG[kBatch];   // mx, my, a, b
-    __shared__ float2 sT[kBatch];   // c, tau
-    __shared__ float4 sW[kBatch];   // sigma, r, g, b
+    // batch arrays at a 16-byte stride, one array after the other, so one
+    // address register per splat reaches all three (immediate offsets)
+    __shared__ __align__(16) float4 sB[3 * kBatch];   // G: mx, my, a, b | W: sigma, r, g, b | T: c, tau
+    float4* const sG = sB;
+    float4* const sW = sB + kBatch;
+    float4* const sT = sB + 2 * kBatch;
     __shared__ uint8_t smask[kBatch];
+    const uint32_t s_base = (uint32_t)__cvta_generic_to_shared(sB);
     __shared__ unsigned long long ssum[kRenderThreads / 32], ssq[kRenderThreads / 32];
     __shared__ int smin[kRenderThreads / 32], smax[kRenderThreads / 32];
     const int tile = order ? (int)order[blockIdx.x] : (int)blockIdx.x;
@@ -127,7 +152,7 @@ k_render(Src src, const int64_t* __restrict__ ranges, int32_t width, int32_t hei
         for (int i = threadIdx.x; i < nb; i += kRenderThreads) {
             const Record r = src.load(b + i);
             sG[i] = r.a;
-            sT[i] = make_float2(r.b.x, r.c.y);
+            sT[i] = make_float4(r.b.x, r.c.y, 0.f, 0.f);
             sW[i] = make_float4(r.b.y, r.b.z, r.b.w, r.c.x);
             smask[i] = (uint8_t)warp_mask(r, x_lo, y_lo);
         }
@@ -138,11 +163,12 @@ k_render(Src src, const int64_t* __restrict__ ranges, int32_t width, int32_t hei
                 while (m) {
                     const int j = c0 + __ffs(m) - 1;
                     m &= m - 1u;
-                    const float4 G = sG[j];
-                    const float2 Tc = sT[j];
+                    const uint32_t sa = s_base + 16u * j;
+                    const float4 G = lds_f4<0>(sa);
+                    const float2 Tc = lds_f2<2 * 16 * kBatch>(sa);
                     const float tau = Tc.y;
                     if (tau < -3.0e38f) {  // slow splat: full exp_np, scalar per pixel
-                        const float4 W = sW[j];
+                        const float4 W = lds_f4<16 * kBatch>(sa);
                         float t0 = lo_of(T), t1 = hi_of(T);
                         float a0 = lo_of(C0), a1 = hi_of(C0), b0 = lo_of(C1), b1 = hi_of(C1);
                         float d0 = lo_of(C2), d1 = hi_of(C2);
@@ -167,7 +193,7 @@ k_render(Src src, const int64_t* __restrict__ ranges, int32_t width, int32_t hei
                     bool p0 = !DONE0 && lo_of(pw) >= tau;
                     bool p1 = !DONE1 && hi_of(pw) >= tau;
                     if (!(p0 || p1)) continue;  // both alphas < alpha_low for sure
-                    const float4 W = sW[j];
+                    const float4 W = lds_f4<16 * kBatch>(sa);
                     const f2 al = mul2(bc(W.x), exp2_np_fast(pw, K), K);
                     float a0 = fminf(lo_of(al), 0.99f), a1 = fminf(hi_of(al), 0.99f);  // finite here
                     p0 = p0 && a0 >= alpha_low;
@@ -182,8 +208,8 @@ k_render(Src src, const int64_t* __restrict__ ranges, int32_t width, int32_t hei
                     C1 = add2(C1, mul2(w, bc(W.z), K), K);
                     C2 = add2(C2, mul2(w, bc(W.w), K), K);
                     T = mul2(T, sub2(K.one, A, K), K);
-                    cnt0 += p0;
-                    cnt1 += p1;
+                    inc_if(cnt0, p0);
+                    inc_if(cnt1, p1);
                     if (kFlagDone) {
                         if (p0 && lo_of(T) < term) fdone0 = true;
                         if (p1 && hi_of(T) < term) fdone1 = true;
