@@ -16,6 +16,15 @@
 
 namespace adr {
 
+#ifdef ADR_RENDER_PROFILE
+// opt-in build (EXTRA_NVFLAGS=-DADR_RENDER_PROFILE, tools/render_profile.py):
+// warp-iteration outcome counters of the blend loop
+__device__ unsigned long long g_render_prof[8];
+#define RPROF(i, v) rp[i] += (v)
+#else
+#define RPROF(i, v) ((void)0)
+#endif
+
 namespace {
 
 constexpr int kRenderThreads = 128;       // 2 pixels per thread
@@ -23,7 +32,7 @@ constexpr int kBatch = 256;               // pairs staged per round
 
 // Record source for the fused frame: records by rank + per-pair rank list.
 struct RecSource {
-    static constexpr int kMinBlocks = 8;   // 64 registers
+    static constexpr int kMinBlocks = 7;   // 72 registers
     const Record* rec;
     const uint32_t* idx;
     __device__ __forceinline__ Record load(int64_t j) const { return rec[idx[j]]; }
@@ -77,11 +86,69 @@ __device__ __forceinline__ float2 lds_f2(uint32_t a) {
 // mask is set when the splat's conservative box (mx +- hx, my +- hy) meets the
 // quadrant's pixel columns and rows.
 __device__ __forceinline__ uint32_t warp_mask(const Record& r, float x_lo, float y_lo) {
+    // pixel centres are integers: only the integer columns ceil(l)..floor(r)
+    // and rows ceil(t)..floor(b) of the box can contribute, so a box that
+    // straddles no pixel centre of a quadrant (small splats between centres)
+    // does not enter it (each pixel's own test is unchanged: px >= l <=>
+    // px >= ceil(l) for integer px)
     const float mx = r.a.x, my = r.a.y, hx = r.c.z, hy = r.c.w;
-    const float l = mx - hx, rr = mx + hx, t = my - hy, b = my + hy;
+    const float l = ceilf(mx - hx), rr = floorf(mx + hx), t = ceilf(my - hy), b = floorf(my + hy);
+    if (!(l <= rr && t <= b)) return 0u;
     const uint32_t xm = (uint32_t)(l <= x_lo + 7.0f && rr >= x_lo) | ((uint32_t)(l <= x_lo + 15.0f && rr >= x_lo + 8.0f) << 1);
     const uint32_t ym = (uint32_t)(t <= y_lo + 7.0f && b >= y_lo) | ((uint32_t)(t <= y_lo + 15.0f && b >= y_lo + 8.0f) << 1);
     return (xm * ((ym & 1u) | ((ym & 2u) << 1)));  // bits: (qy,qx) = 0:(0,0) 1:(0,1) 2:(1,0) 3:(1,1)
+}
+
+// warp_mask refined by the tau-ellipse itself: for each 8-row band of the
+// tile, the x-extent of the ellipse over the band's pixel rows (concave in y:
+// the rightmost point if its row lies inside the band, otherwise the larger
+// of the two band-end rows; leftmost alike), widened by a margin far above
+// the evaluation error, decides which column halves can hold a
+// contributing pixel.  The ellipse is Q(d) <= K' with K' = hx^2 det / c: the
+// same inflated ellipse whose x half-extent is hx, so it contains every pixel
+// whose fp32 power reaches tau (cull_params).  Slow splats keep the box.
+__device__ __forceinline__ float sqrt_approx(float x) {
+    float y;
+    asm("sqrt.approx.f32 %0, %1;" : "=f"(y) : "f"(x));
+    return y;
+}
+
+__device__ __forceinline__ uint32_t quad_mask(const Record& r, float x_lo, float y_lo) {
+    const uint32_t m = warp_mask(r, x_lo, y_lo);
+    if (m == 0u || !(r.c.y > -3.0e38f)) return m;
+    const float hx = r.c.z;
+    // per-splat constants in fp64 (det cancels), then fp32: every fp32 error
+    // below is a few ulp of aK or of the extents, far inside eps
+    const double a = r.a.z, b = r.a.w, c = r.b.x;
+    const double det64 = a * c - b * b;
+    if (!(det64 > 0.0 && a > 0.0 && c > 0.0 && hx < 1e30f)) return m;
+    const float det = (float)det64;
+    const float aK = (float)(a * ((double)hx * (double)hx * det64 / c));
+    const float dyr = (float)(-b * (double)hx / c);   // row offset of the rightmost point (leftmost: -dyr)
+    const float ia = (float)(1.0 / a), bf = r.a.w;
+    const float mx = r.a.x, my = r.a.y;
+    const float eps = 1e-3f + 2e-3f * hx + 4e-6f * fabsf(mx);
+    const float t = ceilf(my - r.c.w), bt = floorf(my + r.c.w);
+    uint32_t out = 0u;
+#pragma unroll
+    for (int band = 0; band < 2; ++band) {
+        const uint32_t bits = m & (3u << (2 * band));
+        if (!bits) continue;
+        const float d0 = fmaxf(y_lo + 8.0f * band, t) - my;
+        const float d1 = fminf(y_lo + 8.0f * band + 7.0f, bt) - my;
+        const float D0 = aK - det * d0 * d0, D1 = aK - det * d1 * d1;
+        float xr = hx, xl = -hx;
+        if (D0 >= 0.0f && D1 >= 0.0f) {
+            const float s0 = sqrt_approx(D0), s1 = sqrt_approx(D1);
+            if (!(dyr >= d0 && dyr <= d1)) xr = fmaxf(-bf * d0 + s0, -bf * d1 + s1) * ia;
+            if (!(-dyr >= d0 && -dyr <= d1)) xl = fminf(-bf * d0 - s0, -bf * d1 - s1) * ia;
+        }
+        const float L = ceilf(mx + xl - eps), R = floorf(mx + xr + eps);
+        if (!(L <= R)) continue;
+        const uint32_t xm = (uint32_t)(L <= x_lo + 7.0f && R >= x_lo) | ((uint32_t)(L <= x_lo + 15.0f && R >= x_lo + 8.0f) << 1);
+        out |= bits & (xm << (2 * band));
+    }
+    return out;
 }
 
 // One pixel's blend step with the full exp_np (slow splats).
@@ -144,6 +211,9 @@ k_render(Src src, const int64_t* __restrict__ ranges, int32_t width, int32_t hei
     f2 T = kFlagDone ? K.one : pk(in0 ? 1.0f : 0.0f, in1 ? 1.0f : 0.0f), C0 = 0ull, C1 = 0ull, C2 = 0ull;
     int cnt0 = 0, cnt1 = 0;
     bool fdone0 = !in0, fdone1 = !in1;
+#ifdef ADR_RENDER_PROFILE
+    unsigned long long rp[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+#endif
 #define DONE0 (kFlagDone ? fdone0 : lo_of(T) < term)
 #define DONE1 (kFlagDone ? fdone1 : hi_of(T) < term)
     for (int64_t b = start; b < end; b += kBatch) {
@@ -154,15 +224,27 @@ k_render(Src src, const int64_t* __restrict__ ranges, int32_t width, int32_t hei
             sG[i] = r.a;
             sT[i] = make_float4(r.b.x, r.c.y, 0.f, 0.f);
             sW[i] = make_float4(r.b.y, r.b.z, r.b.w, r.c.x);
-            smask[i] = (uint8_t)warp_mask(r, x_lo, y_lo);
+#ifdef ADR_RENDER_PROFILE
+            smask[i] = (uint8_t)(quad_mask(r, x_lo, y_lo) | (warp_mask(r, x_lo, y_lo) << 4));
+#else
+            smask[i] = (uint8_t)quad_mask(r, x_lo, y_lo);
+#endif
         }
         __syncthreads();
+        RPROF(6, 1);
         if (__any_sync(kFull, !(DONE0 && DONE1))) {
             for (int c0 = 0; c0 < nb; c0 += 32) {
+#ifdef ADR_RENDER_PROFILE
+                const uint32_t qm = __ballot_sync(kFull, c0 + lane < nb && ((smask[c0 + lane] >> warp) & 1u));
+                uint32_t m = __ballot_sync(kFull, c0 + lane < nb && ((smask[c0 + lane] >> (4 + warp)) & 1u));
+#else
                 uint32_t m = __ballot_sync(kFull, c0 + lane < nb && ((smask[c0 + lane] >> warp) & 1u));
+#endif
                 while (m) {
                     const int j = c0 + __ffs(m) - 1;
                     m &= m - 1u;
+                    RPROF(0, 1);
+                    RPROF(3, (unsigned)!DONE0 + (unsigned)!DONE1);
                     const uint32_t sa = s_base + 16u * j;
                     const float4 G = lds_f4<0>(sa);
                     const float2 Tc = lds_f2<2 * 16 * kBatch>(sa);
@@ -192,12 +274,23 @@ k_render(Src src, const int64_t* __restrict__ ranges, int32_t width, int32_t hei
                     const f2 pw = sub2(mul2(bc(-0.5f), q, K), bd, K);
                     bool p0 = !DONE0 && lo_of(pw) >= tau;
                     bool p1 = !DONE1 && hi_of(pw) >= tau;
+                    RPROF(4, (unsigned)p0 + (unsigned)p1);
+                    RPROF(1, __all_sync(kFull, !(p0 || p1)));
+                    RPROF(7, __all_sync(kFull, !(p0 || p1)) && __all_sync(kFull, !DONE0 && !DONE1));
+#ifdef ADR_RENDER_PROFILE
+                    // slot 2: iterations quad_mask removes; slot 6 += 1e9 per unsafe removal
+                    if (!((qm >> (j - c0)) & 1u)) {
+                        RPROF(2, lane == 0);
+                        if (__any_sync(kFull, p0 || p1) && lane == 0) rp[6] += 1000000000ull;
+                    }
+#endif
                     if (!(p0 || p1)) continue;  // both alphas < alpha_low for sure
                     const float4 W = lds_f4<16 * kBatch>(sa);
                     const f2 al = mul2(bc(W.x), exp2_np_fast(pw, K), K);
                     float a0 = fminf(lo_of(al), 0.99f), a1 = fminf(hi_of(al), 0.99f);  // finite here
                     p0 = p0 && a0 >= alpha_low;
                     p1 = p1 && a1 >= alpha_low;
+                    RPROF(5, (unsigned)p0 + (unsigned)p1);
                     if (!(p0 || p1)) continue;
                     // a lane that does not contribute blends alpha = 0 — an exact
                     // no-op (T * 1 = T, C + 0 * colour = C for finite colours),
@@ -221,6 +314,15 @@ k_render(Src src, const int64_t* __restrict__ ranges, int32_t width, int32_t hei
     }
 #undef DONE0
 #undef DONE1
+#ifdef ADR_RENDER_PROFILE
+    // per-warp events (0, 1, 2, 6) counted once per warp; per-pixel sums (3, 4, 5) summed over lanes
+    for (int k = 0; k < 8; ++k) {
+        unsigned long long v = rp[k];
+        if (k == 3 || k == 4 || k == 5)
+            for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(kFull, v, o);
+        if (lane == 0) atomicAdd(&g_render_prof[k], v);
+    }
+#endif
     const float t0 = lo_of(T), t1 = hi_of(T);
     const float o[2][3] = {{__fadd_rn(lo_of(C0), __fmul_rn(t0, bg0)), __fadd_rn(lo_of(C1), __fmul_rn(t0, bg1)),
                             __fadd_rn(lo_of(C2), __fmul_rn(t0, bg2))},
@@ -364,3 +466,13 @@ int32_t launch_render_proj(const adr_projection& p, const int64_t* gidx, const i
 }
 
 }  // namespace adr
+
+#ifdef ADR_RENDER_PROFILE
+extern "C" int32_t adr_debug_render_profile(unsigned long long* host_out) {
+    cudaDeviceSynchronize();
+    cudaMemcpyFromSymbol(host_out, adr::g_render_prof, sizeof(unsigned long long) * 8);
+    unsigned long long z[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+    cudaMemcpyToSymbol(adr::g_render_prof, z, sizeof(z));
+    return 0;
+}
+#endif

@@ -472,3 +472,21 @@ def test_term_threshold_vs_oracle(oracle, term):
     img, load = ab.render(proj, pairs, grid, cam, ab.ALPHA_LOW, term_threshold=term)
     assert bits_equal(_np(img.pixels), ref["pixels"])
     assert np.array_equal(_np(load.counts), ref["load"])
+
+
+@pytest.mark.parametrize("seed,aniso,scales,mode", [
+    (81, (10.0, 60.0), (0.002, 0.05), "aabb"),      # needle-like splats at every orientation
+    (82, (1.0, 1.2), (0.0005, 0.004), "circle"),    # sub-pixel splats between pixel centres
+    (83, (2.0, 30.0), (0.05, 0.4), "baseline"),     # large sheared splats spanning many tiles
+])
+def test_quadrant_culling_extreme_shapes_vs_oracle(oracle, seed, aniso, scales, mode):
+    """The render skips a warp's 8x8 quadrant for a splat only when the
+    splat's tau-ellipse provably misses the quadrant's pixel centres
+    (quad_mask); extreme anisotropy, sub-pixel and huge splats stress that
+    bound.  Bit-exact image and load map against the oracle."""
+    import paper_2409_08669_b200 as ab
+
+    spec = ab.SyntheticSpec(extent=1.0, scale_range=scales, anisotropy_range=aniso, opacity_range=(0.02, 1.0))
+    a = ab.synthetic_arrays(seed, 30000, spec, sh_degree=1)
+    cam = ab.Camera.from_lookat((0.4, -0.3, -2.5), (0, 0, 0), width=203, height=157, background=(0.0, 0.1, 0.2))
+    _oracle_check(oracle, a, 1, cam, mode)
