@@ -376,15 +376,34 @@ def run_ours(args, cfg, rank, world, local):
         torch.cuda.synchronize(dev)
         if dist:
             dist.barrier()
+        # two device copies of the scene: the H2D copy of step s+1's scene (copy
+        # stream) overlaps step s's frame and D2H (compute stream); every step
+        # still moves its own inputs in and its own result out
+        dst2 = [t.clone() for t in dst]
+        ds2 = ab.DeviceScene(*dst2, sh_degree=ds.sh_degree)
+        n_e2e_views = min(len(mine), 4)
+        eg = [[rast.capture(d, mine[v], mode=cfg["mode"]) for v in range(n_e2e_views)] for d in (ds, ds2)]
+        bufs = [dst, dst2]
+        cstream = torch.cuda.Stream(dev)
+        ready = [torch.cuda.Event(), torch.cuda.Event()]
+        free = [torch.cuda.Event(), torch.cuda.Event()]
+        torch.cuda.synchronize(dev)
         a0, a1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         a0.record(stream)
+        cstream.wait_event(a0)
         for s in range(k_e2e):
-            for a, b in zip(dst, src):
-                a.copy_(b, non_blocking=True)
-            v = s % len(graphs)
-            graphs[v].replay()
-            img_h.copy_(rasts[v % n_fly].pixels, non_blocking=True)
-            load_h.copy_(rasts[v % n_fly].load, non_blocking=True)
+            bb = s % 2
+            with torch.cuda.stream(cstream):
+                if s >= 2:
+                    cstream.wait_event(free[bb])
+                for a, b in zip(bufs[bb], src):
+                    a.copy_(b, non_blocking=True)
+                ready[bb].record(cstream)
+            stream.wait_event(ready[bb])
+            eg[bb][s % n_e2e_views].replay()
+            img_h.copy_(rast.pixels, non_blocking=True)
+            load_h.copy_(rast.load, non_blocking=True)
+            free[bb].record(stream)
         a1.record(stream)
         torch.cuda.synchronize(dev)
         ems = a0.elapsed_time(a1)
@@ -406,7 +425,8 @@ def run_ours(args, cfg, rank, world, local):
         e2e = {"value": world * k_e2e / (ems * 1e-3), "unit": "frames/s",
                "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
                "path": "Rasterizer frame via the C-ABI with the scene copied from pinned host "
-                       "memory every step and image+load map copied back (run_pipeline semantics)"}
+                       "memory every step and image+load map copied back (run_pipeline semantics); "
+                       "double-buffered device scene: step s+1's H2D copy overlaps step s's frame"}
         e2e_res = {"value": world * args.steps / (rms * 1e-3), "unit": "frames/s",
                    "h2d_bytes_per_step": ctypes.sizeof(_lib.Camera_t), "d2h_bytes_per_step": d2h,
                    "path": "resident scene, camera in, image+load map out (serving)"}
