@@ -473,6 +473,11 @@ def run_ours(args, cfg, rank, world, local):
                        "views_in_flight": n_fly},
             "pairs_per_frame": p_mean,
             "stages_ms": med,
+            # sort rates (BASELINE north_star asks for keys/s): the tile sort is the
+            # stable 2-pass radix of the P (tile, Gaussian) pairs; the "inclusivesum"
+            # stage is the depth-rank sort of the N Gaussians plus the pair-offset scan
+            "sort_rates": {"tile_sort_pairs_per_s": p_mean / (med["sort"] * 1e-3),
+                           "depth_sort_and_offsets_keys_per_s": cfg["n"] / (med["inclusivesum"] * 1e-3)},
             "load_stats": {"mean": load_stats.mean, "std": load_stats.std, "min": load_stats.min,
                            "max": load_stats.max},
             # the longest kernel of the frame, and HBM-bound: the fp64 preprocess
