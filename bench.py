@@ -352,7 +352,7 @@ def run_ours(args, cfg, rank, world, local):
     # are the scene read, the Projection write and the render records of the
     # surviving Gaussians
     alive = cfg["n"] - culled
-    pre_bytes = cfg["n"] * (44 + 12 * k_sh) + cfg["n"] * (65 + 4) + alive * (48 + 16)
+    pre_bytes = cfg["n"] * (44 + 12 * k_sh) + cfg["n"] * (65 + 4) + alive * (48 + 8)
     pre_gbs = pre_bytes / (med["preprocess"] * 1e-3) / 1e9
 
     # e2e 1: the drop-in call — scene from pinned host memory each step, frame,

@@ -244,17 +244,17 @@ k_scan_lookback(Op op, const int64_t* d_n, int64_t n_static, uint64_t* status, u
 }
 
 // Pair offsets in rank order: off[r] = sum_{r' < r} count(r'), where
-// count(r) is the area of rinfo[r]'s tile rectangle; clamped to the pair
+// count(r) is the area of rect[r]'s tile rectangle; clamped to the pair
 // capacity, and off[M] = min(P, cap) closes the table.
 struct RankOffsetsOp {
-    const uint4* rinfo;
+    const uint2* rect;
     uint32_t* off;
     const int64_t* d_m;
     int64_t* d_p;        // true pair count
     int64_t* d_pc;       // pair count clamped to capacity
     int64_t cap;
     __device__ uint64_t load(int64_t r) const {
-        const uint4 inf = rinfo[r];
+        const uint2 inf = rect[r];
         return (uint64_t)((inf.x >> 16) - (inf.x & 0xffffu)) * ((inf.y >> 16) - (inf.y & 0xffffu));
     }
     __device__ void store(int64_t r, uint64_t ex, uint64_t) const {
@@ -281,7 +281,8 @@ struct RankOffsetsOp {
 // start offsets, so lanes do equal work however uneven the rectangles are.
 template <typename TileT>
 __global__ void __launch_bounds__(256)
-k_emit_balanced(const uint4* __restrict__ rinfo, const uint32_t* __restrict__ off, const int64_t* __restrict__ d_m,
+k_emit_balanced(const uint2* __restrict__ rect, const uint32_t* __restrict__ order, const uint32_t* __restrict__ off,
+                const int64_t* __restrict__ d_m,
                 const int64_t* __restrict__ d_pc, int32_t tiles_x, TileT* __restrict__ tiles, uint32_t* __restrict__ gs) {
     const int lane = threadIdx.x & 31;
     const uint32_t m = (uint32_t)*d_m;
@@ -290,7 +291,8 @@ k_emit_balanced(const uint4* __restrict__ rinfo, const uint32_t* __restrict__ of
     if (r0 >= m) return;
     const uint32_t r = r0 + lane;
     const bool valid = r < m;
-    const uint4 inf = valid ? rinfo[r] : make_uint4(0, 0, 0, 0);
+    const uint2 inf = valid ? rect[r] : make_uint2(0, 0);
+    const uint32_t gidx = valid ? order[r] : 0u;
     const uint32_t o = valid ? off[r] : pc;
     const uint32_t wstart = __shfl_sync(kFull, o, 0);
     uint32_t wend = r0 + 32 < m ? off[r0 + 32] : pc;
@@ -311,7 +313,7 @@ k_emit_balanced(const uint4* __restrict__ rinfo, const uint32_t* __restrict__ of
         const uint32_t wL = __shfl_sync(kFull, w, L);
         const float rwL = __shfl_sync(kFull, rw, L);
         const uint32_t xyL = __shfl_sync(kFull, xy0, L);
-        const uint32_t gL = __shfl_sync(kFull, inf.z, L);
+        const uint32_t gL = __shfl_sync(kFull, gidx, L);
         if (q < wend) {
             const uint32_t j = q - oL;
             uint32_t row = (uint32_t)((float)j * rwL);
@@ -374,7 +376,7 @@ size_t frame_binning_scratch(int64_t n, int64_t cap, int64_t n_tiles) {
     const size_t tile_sz = wide ? 4 : 2;
     size_t s = 0;
     s += align_up(4 * (size_t)n) + align_up(4 * (size_t)(n + 1));      // skey, off
-    s += align_up(16 * (size_t)n);                                     // rinfo
+    s += align_up(8 * (size_t)n);                                      // rect by rank
     s += radix_scratch_bytes<uint32_t, uint32_t>(n);
     s += lookback_bytes(nlb);
     s += 2 * align_up(tile_sz * (size_t)cap) + align_up(4 * (size_t)cap);  // tiles, sorted tiles, gs
@@ -388,7 +390,7 @@ static int32_t frame_binning_t(const FrameBinning& fb, cudaStream_t st) {
     const int64_t n = fb.n, cap = fb.cap;
     uint32_t* skey = c.take<uint32_t>(n);
     uint32_t* off = c.take<uint32_t>(n + 1);
-    uint4* rinfo = c.take<uint4>(n);
+    uint2* rect = c.take<uint2>(n);
     void* rs1 = c.take<char>((int64_t)radix_scratch_bytes<uint32_t, uint32_t>(n));
     const int64_t nlb = ceil_div(n, kLbTile);
     uint64_t* st2 = c.take<uint64_t>(nlb + 1);
@@ -403,17 +405,17 @@ static int32_t frame_binning_t(const FrameBinning& fb, cudaStream_t st) {
     //     (float32 depth bits, all-ones for Gaussians without pairs) with
     //     the identity as values: ranks [0, M) are the Gaussians with pairs
     //     ordered by (depth bits, index); the last pass writes, per rank,
-    //     rinfo = (x-range, y-range, Gaussian index, depth bits)
+    //     order[rank] = Gaussian index and rect[rank] = its tile rectangle
     SortExtra dx;
     dx.mode = 2;
     dx.gsrc = fb.gpack;
-    dx.gdst = rinfo;
+    dx.gdst = rect;
     int32_t rc = radix_sort<uint32_t, uint32_t>(fb.dkey, nullptr, skey, fb.order, nullptr, n, 32, rs1,
                                                 radix_scratch_bytes<uint32_t, uint32_t>(n), st, dx);
     if (rc) return rc;
     // (c) pair offsets in rank order, and P
     ADR_CUDA_TRY(cudaMemsetAsync(st2, 0, sizeof(uint64_t) * (nlb + 1), st));
-    RankOffsetsOp oo{rinfo, off, ctr + 2, ctr + 0, ctr + 3, cap};
+    RankOffsetsOp oo{rect, off, ctr + 2, ctr + 0, ctr + 3, cap};
     k_scan_lookback<RankOffsetsOp><<<nlb, kLbBlock, 0, st>>>(oo, ctr + 2, n, st2,
                                                             reinterpret_cast<unsigned long long*>(st2 + nlb));
     ADR_LAUNCH_CHECK();
@@ -422,7 +424,8 @@ static int32_t frame_binning_t(const FrameBinning& fb, cudaStream_t st) {
     int tbits = 0;
     while ((int64_t(1) << tbits) < fb.n_tiles) ++tbits;
     if (tbits == 0) tbits = 1;
-    k_emit_balanced<TileT><<<ceil_div(n, 256), 256, 0, st>>>(rinfo, off, ctr + 2, ctr + 3, fb.tiles_x, tiles, gs);
+    k_emit_balanced<TileT><<<ceil_div(n, 256), 256, 0, st>>>(rect, fb.order, off, ctr + 2, ctr + 3, fb.tiles_x,
+                                                              tiles, gs);
     ADR_LAUNCH_CHECK();
     if (fb.ev_after_dup) ADR_CUDA_TRY(cudaEventRecord(fb.ev_after_dup, st));
     // (e) stable radix sort by tile id; the last pass writes the sorted

@@ -28,7 +28,7 @@ struct FrameBinning {
     int64_t n_tiles = 0;
     int32_t tiles_x = 0, tiles_y = 0;
     const uint32_t* dkey = nullptr;  // stage 1 depth-sort key (all-ones: no pairs)
-    const uint4* gpack = nullptr;  // per-Gaussian packed rect + depth bits (stage 1)
+    const uint2* gpack = nullptr;  // per-Gaussian packed tile rect (stage 1)
     uint32_t* order = nullptr;  // scratch: order[rank] = Gaussian index
     int64_t* ranges = nullptr;  // out: (n_tiles, 2)
     uint64_t* keys = nullptr;   // optional out: sorted keys (tile << 32 | depth bits)

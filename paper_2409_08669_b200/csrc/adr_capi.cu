@@ -32,7 +32,7 @@ struct FrameLayout {
     uint32_t* dkey;
     uint32_t* order;
     Record* rec;
-    uint4* gpack;
+    uint2* gpack;
     uint32_t* tile_order;
     void* binning;
     size_t binning_bytes;
@@ -44,7 +44,7 @@ size_t frame_bytes(int64_t n, int64_t n_tiles, int64_t cap, FrameLayout* out, vo
     l.dkey = c.take<uint32_t>(n);
     l.order = c.take<uint32_t>(n);
     l.rec = c.take<Record>(n);
-    l.gpack = c.take<uint4>(n);
+    l.gpack = c.take<uint2>(n);
     l.tile_order = c.take<uint32_t>(n_tiles);
     l.binning_bytes = frame_binning_scratch(n, cap, n_tiles);
     l.binning = c.take<char>((int64_t)l.binning_bytes);

@@ -72,7 +72,7 @@ __device__ inline void cull_params(float a, float b, float c, float op, float al
 // Extra per-Gaussian outputs the fused frame needs from stage 1.
 struct FusedPre {
     Record* rec = nullptr;                    // render record (valid rows)
-    uint4* gpack = nullptr;                   // (x0 | x1 << 16, y0 | y1 << 16, 0, depth bits)
+    uint2* gpack = nullptr;                   // tile rect (x0 | x1 << 16, y0 | y1 << 16)
     unsigned long long* culled = nullptr;     // += number of !valid rows
     uint32_t* dkey = nullptr;                 // depth-sort key (all-ones: no pairs)
     int64_t* d_m = nullptr;                   // += number of Gaussians with pairs (zeroed)

@@ -258,8 +258,8 @@ k_preprocess(const T* __restrict__ centers, const T* __restrict__ scales,
                 R.b = make_float4(cc, op, c0f, c1f);
                 R.c = make_float4(c2f, tau, hx, hy);
                 fused.rec[i] = R;
-                fused.gpack[i] = make_uint4((uint32_t)r.x0 | ((uint32_t)r.x1 << 16),
-                                            (uint32_t)r.y0 | ((uint32_t)r.y1 << 16), 0u, __float_as_uint(dz));
+                fused.gpack[i] = make_uint2((uint32_t)r.x0 | ((uint32_t)r.x1 << 16),
+                                            (uint32_t)r.y0 | ((uint32_t)r.y1 << 16));
             }
         } else {
             reinterpret_cast<float2*>(out.d_mean2d)[i] = make_float2(0.f, 0.f);

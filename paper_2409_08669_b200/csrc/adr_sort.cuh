@@ -122,13 +122,13 @@ scan_u32_exclusive(uint32_t* __restrict__ data, int64_t n, uint64_t* status, uns
 // so (round, lane) order is input order).  vals_in == nullptr means the
 // identity (value = input index).  Last-pass extras (MODE):
 //   1: exp_keys[g] = key << 32 | float bits of exp_depth[value]  (reference keys)
-//   2: gdst[g] = gsrc[value] with .z = value, and no key/value output
+//   2: gdst[g] = gsrc[value] (8-byte gather) and vals_out[g] = value; no key output
 struct SortExtra {
     int mode = 0;
     const float* exp_depth = nullptr;
     uint64_t* exp_keys = nullptr;
-    const uint4* gsrc = nullptr;
-    uint4* gdst = nullptr;
+    const uint2* gsrc = nullptr;
+    uint2* gdst = nullptr;
 };
 
 template <typename K, typename V, int RB, int MODE>
@@ -215,9 +215,8 @@ radix_downsweep(const K* __restrict__ keys_in, const V* __restrict__ vals_in, K*
         const V val = svals[i];
         const int64_t g = goff[digit_of(key, bit, R - 1)] + i;
         if (MODE == 2) {
-            uint4 inf = ex.gsrc[val];
-            inf.z = (uint32_t)val;
-            ex.gdst[g] = inf;
+            vals_out[g] = val;
+            ex.gdst[g] = ex.gsrc[val];
         } else {
             keys_out[g] = key;
             vals_out[g] = val;
