@@ -487,6 +487,9 @@ def run_ours(args, cfg, rank, world, local):
             "render_kernel": {"bound": "fma-pipe", "kernel": "k_render",
                               "gather_gbs": render_gbs, "bytes_per_launch": rbytes, "traffic": traffic,
                               "fma_pipe_active": ncu.get("k_render_fma_pipe"),
+                              "issue_active": ncu.get("k_render_issue_active"),
+                              "warp_inst_per_s": ncu.get("k_render_warp_inst_per_s"),
+                              "warp_inst_peak_per_s": 148 * 4 * clk.get("sm_mhz", 1965.0) * 1e6 if clk else None,
                               "note": "52 B/pair record gathers + outputs, served from L2 (traffic = DRAM "
                                       "bytes per launch); the limiter is FP32 issue for the exact numpy exp "
                                       "(FFMA2 + MUFU) and dependency latency, not memory"},

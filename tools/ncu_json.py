@@ -36,12 +36,19 @@ def main(config, csv_path, rep=None):
     e["k_preprocess_dram_bytes"] = b.get("k_preprocess")
     e["source"] = str(csv_path)
     if rep:
+        ms = ["sm__pipe_fma_cycles_active.avg.pct_of_peak_sustained_active",
+              "smsp__issue_active.avg.pct_of_peak_sustained_active", "smsp__inst_executed.sum",
+              "gpu__time_duration.sum"]
         txt = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv", "--kernel-name", "regex:k_render",
-                              "--metrics", "sm__pipe_fma_cycles_active.avg.pct_of_peak_sustained_active"],
-                             capture_output=True, text=True).stdout
+                              "--metrics", ",".join(ms)], capture_output=True, text=True).stdout
         rows = list(csv.reader(io.StringIO(txt)))
-        i = rows[0].index("sm__pipe_fma_cycles_active.avg.pct_of_peak_sustained_active")
-        e["k_render_fma_pipe"] = float(rows[2][i]) / 100.0
+        val = {m: float(rows[2][rows[0].index(m)].replace(",", "")) for m in ms}
+        dur_s = val["gpu__time_duration.sum"] * {"nsecond": 1e-9, "ns": 1e-9, "usecond": 1e-6, "us": 1e-6, "msecond": 1e-3, "ms": 1e-3}.get(
+            rows[1][rows[0].index("gpu__time_duration.sum")], 1e-9)
+        e["k_render_fma_pipe"] = val[ms[0]] / 100.0
+        e["k_render_issue_active"] = val[ms[1]] / 100.0
+        # warp instructions issued per second (peak: 148 SMs x 4 schedulers x 1 / clock)
+        e["k_render_warp_inst_per_s"] = val[ms[2]] / dur_s
     OUT.write_text(json.dumps(d, indent=1) + "\n")
     print(json.dumps(d, indent=1))
 
