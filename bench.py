@@ -503,6 +503,7 @@ def run_ours(args, cfg, rank, world, local):
             line["e2e_resident"] = e2e_res
         if gather_ms is not None:
             line["gather_ms"] = gather_ms
+        line["per_rank_fps"] = value / world
         if cpu:
             line["cpu_baseline"] = cpu
         print(json.dumps(line), flush=True)
