@@ -490,3 +490,43 @@ def test_quadrant_culling_extreme_shapes_vs_oracle(oracle, seed, aniso, scales, 
     a = ab.synthetic_arrays(seed, 30000, spec, sh_degree=1)
     cam = ab.Camera.from_lookat((0.4, -0.3, -2.5), (0, 0, 0), width=203, height=157, background=(0.0, 0.1, 0.2))
     _oracle_check(oracle, a, 1, cam, mode)
+
+
+@pytest.mark.parametrize("mode", ["baseline", "aabb"])
+def test_slow_and_degenerate_splats_vs_oracle(oracle, mode):
+    """Splats the render must not take through its fast path (SURVEY App. A.3:
+    exp outside [-87, 88] or non-finite operands): a huge needle (ill-
+    conditioned conic), opacity 1e31, NaN and +inf SH coefficients, negative
+    opacity; mixed into an ordinary scene.  Image equal to the oracle's bit for
+    bit where finite and NaN where the oracle's is NaN; load map exact."""
+    import torch
+
+    import paper_2409_08669_b200 as ab
+
+    a = ab.synthetic_arrays(91, 4000, mixed_spec(), sh_degree=1)
+    a = a._replace(centers=a.centers.copy(), scales=a.scales.copy(), rotations=a.rotations.copy(),
+                   opacities=a.opacities.copy(), sh=a.sh.copy())
+    a.scales[0] = (2.5, 0.0005, 0.0005)                      # needle
+    a.rotations[0] = (0.9238795, 0.0, 0.0, 0.3826834)        # 45 degrees about z
+    a.centers[0] = (0.0, 0.0, 0.0)
+    a.opacities[1] = 1e31                                    # exp(power) * 1e31 overflow range
+    a.sh[2, 0, 1] = np.nan                                   # NaN colour channel
+    a.sh[3, 0, 2] = np.inf                                   # +inf coefficient (clipped to 1)
+    a.opacities[4] = -0.5                                    # never contributes
+    for i in range(5):
+        a.centers[i, 2] = -0.3 + 0.1 * i
+    cam = ab.Camera.from_lookat((0.0, 0.0, -3.0), (0, 0, 0), width=120, height=96, background=(0.2, 0.3, 0.1))
+    ds = ab.DeviceScene.from_arrays(a, 1, "cuda", torch.float64)
+    res = ab.run_pipeline(ds, cam, mode=mode)
+    ref = oracle.run_pipeline(dict(centers=a.centers, scales=a.scales, rotations=a.rotations,
+                                   opacities=a.opacities, sh=a.sh, sh_degree=1), cam, mode)
+    p = res.pairs.to_numpy()
+    assert np.array_equal(p["keys"], ref["keys"])
+    assert np.array_equal(p["gaussian_indices"], ref["gidx"])
+    img = _np(res.image.pixels)
+    want = ref["pixels"]
+    nan = np.isnan(want)
+    assert nan.any()                                          # the NaN splat reached pixels
+    assert np.array_equal(np.isnan(img), nan)
+    assert bits_equal(img[~nan], want[~nan])
+    assert np.array_equal(_np(res.load_map.counts), ref["load"])
