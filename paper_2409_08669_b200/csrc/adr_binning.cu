@@ -300,6 +300,11 @@ k_emit_balanced(const uint2* __restrict__ rect, const uint32_t* __restrict__ ord
     const uint32_t x0 = inf.x & 0xffffu, w = (inf.x >> 16) - x0, y0 = inf.y & 0xffffu;
     const float rw = w ? __frcp_rn((float)w) : 0.0f;
     const uint32_t xy0 = x0 | (y0 << 16);
+    // u16 tile ids (<= 65536 tiles, so every rect area j < 2^16): position j
+    // of a rect is tile t0 + j + row * (tiles_x - w) with row = floor(j / w)
+    // = floor((j + 0.5) * RN(1/w)) exactly — (j + 0.5) / w stays >= 0.5 / w
+    // from an integer, far more than the <= 2 ulp product error
+    const uint32_t t0 = y0 * (uint32_t)tiles_x + x0, dw = (uint32_t)tiles_x - w;
     for (uint32_t base = wstart; base < wend; base += 32) {
         const uint32_t q = base + lane;
         // owner of position q: (ranks starting at or before q) - 1, from a
@@ -310,18 +315,29 @@ k_emit_balanced(const uint2* __restrict__ rect, const uint32_t* __restrict__ ord
         const uint32_t starts = __reduce_or_sync(kFull, (valid && o >= base && d < 32u) ? (1u << d) : 0u);
         const int L = (int)(before + __popc(starts & ((2u << lane) - 1u))) - 1;
         const uint32_t oL = __shfl_sync(kFull, o, L);
-        const uint32_t wL = __shfl_sync(kFull, w, L);
         const float rwL = __shfl_sync(kFull, rw, L);
-        const uint32_t xyL = __shfl_sync(kFull, xy0, L);
         const uint32_t gL = __shfl_sync(kFull, gidx, L);
-        if (q < wend) {
-            const uint32_t j = q - oL;
-            uint32_t row = (uint32_t)((float)j * rwL);
-            int32_t col = (int32_t)j - (int32_t)(row * wL);
-            if (col < 0) { --row; col += (int32_t)wL; }
-            if (col >= (int32_t)wL) { ++row; col -= (int32_t)wL; }
-            tiles[q] = (TileT)(((xyL >> 16) + row) * (uint32_t)tiles_x + (xyL & 0xffffu) + (uint32_t)col);
-            gs[q] = gL;
+        if constexpr (sizeof(TileT) == 2) {
+            const uint32_t tL = __shfl_sync(kFull, t0, L);
+            const uint32_t dL = __shfl_sync(kFull, dw, L);
+            if (q < wend) {
+                const uint32_t j = q - oL;
+                const uint32_t row = (uint32_t)(__fadd_rn((float)j, 0.5f) * rwL);
+                tiles[q] = (TileT)(tL + j + row * dL);
+                gs[q] = gL;
+            }
+        } else {
+            const uint32_t wL = __shfl_sync(kFull, w, L);
+            const uint32_t xyL = __shfl_sync(kFull, xy0, L);
+            if (q < wend) {
+                const uint32_t j = q - oL;
+                uint32_t row = (uint32_t)((float)j * rwL);
+                int32_t col = (int32_t)j - (int32_t)(row * wL);
+                if (col < 0) { --row; col += (int32_t)wL; }
+                if (col >= (int32_t)wL) { ++row; col -= (int32_t)wL; }
+                tiles[q] = (TileT)(((xyL >> 16) + row) * (uint32_t)tiles_x + (xyL & 0xffffu) + (uint32_t)col);
+                gs[q] = gL;
+            }
         }
     }
 }
