@@ -222,11 +222,15 @@ k_scan_lookback(Op op, const int64_t* d_n, int64_t n_static, uint64_t* status, u
     const int64_t base = bid * kLbTile + (int64_t)threadIdx.x * kLbIpt;
     uint64_t v[kLbIpt];
     uint64_t s = 0;
+    const bool full = base + kLbIpt <= n;
+    if (full) {
+        op.load_run(base, v);   // the thread's kLbIpt consecutive items, vector loads
+    } else {
 #pragma unroll
-    for (int k = 0; k < kLbIpt; ++k) {
-        v[k] = base + k < n ? op.load(base + k) : 0ull;
-        s += v[k];
+        for (int k = 0; k < kLbIpt; ++k) v[k] = base + k < n ? op.load(base + k) : 0ull;
     }
+#pragma unroll
+    for (int k = 0; k < kLbIpt; ++k) s += v[k];
     uint64_t btot;
     const uint64_t tpre = block_exclusive_sum<uint64_t, kLbBlock>(s, sred, &btot);
     if (threadIdx.x < 32) {
@@ -235,10 +239,20 @@ k_scan_lookback(Op op, const int64_t* d_n, int64_t n_static, uint64_t* status, u
     }
     __syncthreads();
     uint64_t run = sexcl + tpre;
+    if (full) {
+        uint64_t ex[kLbIpt];
 #pragma unroll
-    for (int k = 0; k < kLbIpt; ++k) {
-        if (base + k < n) op.store(base + k, run, v[k]);
-        run += v[k];
+        for (int k = 0; k < kLbIpt; ++k) {
+            ex[k] = run;
+            run += v[k];
+        }
+        op.store_run(base, ex);
+    } else {
+#pragma unroll
+        for (int k = 0; k < kLbIpt; ++k) {
+            if (base + k < n) op.store(base + k, run, v[k]);
+            run += v[k];
+        }
     }
     if (bid == (int64_t)gridDim.x - 1 && threadIdx.x == kLbBlock - 1) op.total(run);
 }
@@ -259,6 +273,24 @@ struct RankOffsetsOp {
     }
     __device__ void store(int64_t r, uint64_t ex, uint64_t) const {
         off[r] = ex < (uint64_t)cap ? (uint32_t)ex : (uint32_t)cap;
+    }
+    // 8 consecutive ranks starting at a multiple of 8: 4 x 16-byte loads
+    __device__ void load_run(int64_t r, uint64_t* v) const {
+        const uint4* q = reinterpret_cast<const uint4*>(rect + r);
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+            const uint4 t = q[k];
+            v[2 * k] = (uint64_t)((t.x >> 16) - (t.x & 0xffffu)) * ((t.y >> 16) - (t.y & 0xffffu));
+            v[2 * k + 1] = (uint64_t)((t.z >> 16) - (t.z & 0xffffu)) * ((t.w >> 16) - (t.w & 0xffffu));
+        }
+    }
+    __device__ void store_run(int64_t r, const uint64_t* ex) const {
+        uint32_t c[8];
+#pragma unroll
+        for (int k = 0; k < 8; ++k) c[k] = ex[k] < (uint64_t)cap ? (uint32_t)ex[k] : (uint32_t)cap;
+        uint4* q = reinterpret_cast<uint4*>(off + r);
+        q[0] = make_uint4(c[0], c[1], c[2], c[3]);
+        q[1] = make_uint4(c[4], c[5], c[6], c[7]);
     }
     __device__ void total(uint64_t t) const {
         const int64_t pc = t < (uint64_t)cap ? (int64_t)t : cap;
