@@ -207,7 +207,11 @@ int32_t stage_ranges(const uint64_t* keys, int64_t p, int64_t n_tiles, int64_t* 
 
 namespace {
 
-constexpr int kLbBlock = 256, kLbIpt = 8, kLbTile = kLbBlock * kLbIpt;
+#ifndef ADR_LB_IPT
+#define ADR_LB_IPT 8
+#endif
+constexpr int kLbBlock = 256, kLbIpt = ADR_LB_IPT, kLbTile = kLbBlock * kLbIpt;
+static_assert(kLbIpt % 4 == 0, "vector runs of 4 ranks");
 
 // Generic single-pass exclusive scan with decoupled look-back; Op supplies
 // load(i) -> u64, store(i, exclusive, value) and total(sum).
@@ -274,23 +278,23 @@ struct RankOffsetsOp {
     __device__ void store(int64_t r, uint64_t ex, uint64_t) const {
         off[r] = ex < (uint64_t)cap ? (uint32_t)ex : (uint32_t)cap;
     }
-    // 8 consecutive ranks starting at a multiple of 8: 4 x 16-byte loads
+    // kLbIpt consecutive ranks starting at a multiple of kLbIpt: 16-byte loads
     __device__ void load_run(int64_t r, uint64_t* v) const {
         const uint4* q = reinterpret_cast<const uint4*>(rect + r);
 #pragma unroll
-        for (int k = 0; k < 4; ++k) {
+        for (int k = 0; k < kLbIpt / 2; ++k) {
             const uint4 t = q[k];
             v[2 * k] = (uint64_t)((t.x >> 16) - (t.x & 0xffffu)) * ((t.y >> 16) - (t.y & 0xffffu));
             v[2 * k + 1] = (uint64_t)((t.z >> 16) - (t.z & 0xffffu)) * ((t.w >> 16) - (t.w & 0xffffu));
         }
     }
     __device__ void store_run(int64_t r, const uint64_t* ex) const {
-        uint32_t c[8];
+        uint32_t c[kLbIpt];
 #pragma unroll
-        for (int k = 0; k < 8; ++k) c[k] = ex[k] < (uint64_t)cap ? (uint32_t)ex[k] : (uint32_t)cap;
+        for (int k = 0; k < kLbIpt; ++k) c[k] = ex[k] < (uint64_t)cap ? (uint32_t)ex[k] : (uint32_t)cap;
         uint4* q = reinterpret_cast<uint4*>(off + r);
-        q[0] = make_uint4(c[0], c[1], c[2], c[3]);
-        q[1] = make_uint4(c[4], c[5], c[6], c[7]);
+#pragma unroll
+        for (int k = 0; k < kLbIpt / 4; ++k) q[k] = make_uint4(c[4 * k], c[4 * k + 1], c[4 * k + 2], c[4 * k + 3]);
     }
     __device__ void total(uint64_t t) const {
         const int64_t pc = t < (uint64_t)cap ? (int64_t)t : cap;
