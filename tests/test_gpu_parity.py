@@ -530,3 +530,24 @@ def test_slow_and_degenerate_splats_vs_oracle(oracle, mode):
     assert np.array_equal(np.isnan(img), nan)
     assert bits_equal(img[~nan], want[~nan])
     assert np.array_equal(_np(res.load_map.counts), ref["load"])
+
+
+@pytest.mark.parametrize("zspan", [(0.5, 3.0), (0.3, 900.0)])
+def test_depth_key_range_plans_vs_oracle(oracle, zspan):
+    """Narrow and wide depth ranges (depths spread over three decades: the
+    float depth keys then differ in their exponent bits, so every radix pass
+    of the depth sort reorders): keys, Gaussian indices, image and load map
+    equal the reference's stable argsort order."""
+    import paper_2409_08669_b200 as ab
+
+    a = ab.synthetic_arrays(95, 20000, mixed_spec(), sh_degree=1)
+    z0, z1 = zspan
+    rng = np.random.default_rng(3)
+    depth = np.exp(rng.uniform(np.log(z0), np.log(z1), size=len(a.opacities)))
+    centers = a.centers.copy()
+    centers[:, 2] = depth - 3.0                               # camera at z = -3 looking +z
+    centers[:, :2] *= (depth / 3.0)[:, None]                  # stay inside the frustum
+    scales = a.scales * (depth / 3.0)[:, None]
+    a = a._replace(centers=centers, scales=scales)
+    cam = ab.Camera.from_lookat((0.0, 0.0, -3.0), (0, 0, 0), width=160, height=120, background=(0.1, 0.1, 0.1))
+    _oracle_check(oracle, a, 1, cam, "aabb")
