@@ -1,5 +1,6 @@
 """GPU parity at BASELINE.json's full sizes (configs[1] truck 2.5M / 979x546
-circle, configs[2] garden 5.8M / 1297x840 aabb), one orbit view each.
+circle, configs[2] garden 5.8M / 1297x840 aabb, configs[3] playroom 2.3M /
+1264x832 aabb), one orbit view each.
 
 The C oracle (OpenMP over the host cores) finishes a 5.8M frame in seconds,
 so these are full bit-exact comparisons, plus the size-independent
@@ -29,7 +30,7 @@ def _cfg(name):
     return bench.CONFIGS[name], bench
 
 
-@pytest.mark.parametrize("name,view", [("garden", 0), ("truck", 3)])
+@pytest.mark.parametrize("name,view", [("garden", 0), ("truck", 3), ("playroom", 5)])
 def test_fullsize_frame_bitexact_vs_oracle(oracle, name, view):
     import torch
 
