@@ -378,45 +378,34 @@ k_emit_balanced(const uint2* __restrict__ rect, const uint32_t* __restrict__ ord
     }
 }
 
-// ranges[t] = (lower_bound(t), lower_bound(t+1)) over sorted tile ids; each
-// thread owns 16 consecutive positions (two 16-byte loads for u16 ids; the
-// element before them comes from the neighbouring lane) and writes the
-// boundaries that fall on them; position p (the end) is owned by the thread
-// whose range contains it.  Sorted input: a chunk whose first and last ids
-// equal its predecessor's holds no boundary (the common case) and exits.
+// Tile ranges by search instead of a scan of all P sorted tile ids: warp t
+// finds lower_bound(t) with a 32-ary search (each step probes 32 evenly spaced
+// positions of the current interval and keeps the one gap where the ids cross
+// t), so the whole pass reads ~(T + 1) * 32 * log32(P) ids instead of P.
+// ranges[t] = (lb(t), lb(t + 1)); lb(T) = P closes the last tile.
 template <typename TileT>
-__global__ void k_ranges_tiles(const TileT* __restrict__ tiles, const int64_t* __restrict__ d_p, int64_t n_tiles,
-                               int64_t* __restrict__ ranges) {
-    constexpr int kPer = 16;
-    const int64_t p = *d_p;
-    const int64_t i0 = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) * kPer;
-    TileT v[kPer + 1];
-    const bool full = sizeof(TileT) == 2 && i0 + kPer <= p;
-    if (full) {
-        const uint4 q0 = *reinterpret_cast<const uint4*>(tiles + i0);
-        const uint4 q1 = *reinterpret_cast<const uint4*>(tiles + i0 + 8);
-#pragma unroll
-        for (int k = 0; k < 8; ++k) {
-            v[k + 1] = reinterpret_cast<const TileT*>(&q0)[k];
-            v[k + 9] = reinterpret_cast<const TileT*>(&q1)[k];
-        }
-    } else {
-#pragma unroll
-        for (int k = 0; k < kPer; ++k) v[k + 1] = i0 + k < p ? tiles[i0 + k] : TileT(0);
-    }
-    // predecessor: last id of the lane to the left (lane 0 loads it)
+__global__ void __launch_bounds__(256) k_ranges_search(const TileT* __restrict__ tiles, const int64_t* __restrict__ d_p,
+                                                       int64_t n_tiles, int64_t* __restrict__ ranges) {
     const int lane = threadIdx.x & 31;
-    const TileT left = (TileT)__shfl_up_sync(0xffffffffu, (uint32_t)v[kPer], 1);
-    v[0] = lane ? left : (i0 > 0 && i0 - 1 < p ? tiles[i0 - 1] : TileT(0));
-    if (i0 > p) return;
-    if (full && i0 > 0 && v[0] == v[kPer] && i0 + kPer < p) return;
-#pragma unroll
-    for (int k = 0; k < kPer; ++k) {
-        const int64_t i = i0 + k;
-        if (i > p) break;
-        const int64_t prev = i == 0 ? -1 : (int64_t)v[k];
-        const int64_t cur = i < p ? (int64_t)v[k + 1] : n_tiles;
-        if (cur != prev) write_bounds<TileT>(i, prev, cur, n_tiles, ranges);
+    const int64_t t = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    if (t > n_tiles) return;
+    const int64_t p = *d_p;
+    int64_t lo = 0, hi = p;   // lb(t) in [lo, hi]
+    while (hi - lo > 32) {
+        const int64_t step = (hi - lo + 31) / 32;
+        const int64_t q = lo + lane * step;
+        const bool below = q < hi && (int64_t)tiles[q] < t;
+        const int c = __popc(__ballot_sync(kFull, below));
+        const int64_t nlo = c > 0 ? lo + (int64_t)(c - 1) * step + 1 : lo;
+        const int64_t qc = lo + (int64_t)c * step;
+        hi = (c < 32 && qc < hi) ? qc : hi;
+        lo = nlo;
+    }
+    const bool below = lo + lane < hi && (int64_t)tiles[lo + lane] < t;
+    const int64_t lb = lo + __popc(__ballot_sync(kFull, below));
+    if (lane == 0) {
+        if (t < n_tiles) ranges[2 * t] = lb;
+        if (t > 0) ranges[2 * (t - 1) + 1] = lb;
     }
 }
 
@@ -492,7 +481,8 @@ static int32_t frame_binning_t(const FrameBinning& fb, cudaStream_t st) {
     if (rc) return rc;
     if (fb.ev_after_sort) ADR_CUDA_TRY(cudaEventRecord(fb.ev_after_sort, st));
     // (f) tile ranges
-    k_ranges_tiles<TileT><<<ceil_div(ceil_div(cap + 1, 16), 256), 256, 0, st>>>(stiles, ctr + 3, fb.n_tiles, fb.ranges);
+    k_ranges_search<TileT><<<ceil_div((fb.n_tiles + 1) * 32, 256), 256, 0, st>>>(stiles, ctr + 3, fb.n_tiles,
+                                                                                  fb.ranges);
     ADR_LAUNCH_CHECK();
     if (fb.ev_after_ranges) ADR_CUDA_TRY(cudaEventRecord(fb.ev_after_ranges, st));
     return ADR_OK;
