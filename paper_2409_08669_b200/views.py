@@ -76,6 +76,29 @@ def gather_frames(frames, stats, n_views: int, group=None, dst: int = 0):
     return all_f.index_select(0, idx), all_s.index_select(0, idx)
 
 
+def broadcast_scene(scene, n: int, sh_degree: int, device, dtype=None, group=None, src: int = 0):
+    """Replicate a scene from rank `src` on every rank (load
+    once, broadcast N·(44 + 12K) bytes at fp32).  `scene` is the source
+    rank's DeviceScene (ignored elsewhere); every rank passes the same N and
+    SH degree and gets a DeviceScene of its own on `device`."""
+    import torch
+    import torch.distributed as dist
+
+    from .scene import DeviceScene
+
+    dtype = dtype or (scene.centers.dtype if scene is not None else torch.float32)
+    k = (sh_degree + 1) ** 2
+    shapes = [(n, 3), (n, 3), (n, 4), (n,), (n, k, 3)]
+    if dist.get_rank(group) == src:
+        ts = [t.to(device=device, dtype=dtype).contiguous() for t in
+              (scene.centers, scene.scales, scene.rotations, scene.opacities, scene.sh)]
+    else:
+        ts = [torch.empty(sh, dtype=dtype, device=device) for sh in shapes]
+    for t in ts:
+        dist.broadcast(t, src=src, group=group)
+    return DeviceScene(*ts, sh_degree=sh_degree)
+
+
 def pack_frame(pixels, load):
     """(H,W,3) float32 + (H,W) int32 -> (H,W,4) float32 (load stored as bits)."""
     import torch

@@ -109,3 +109,45 @@ def test_gather_frames_gloo_world2(n_views):
         px, ld, st = _fake_view(k, h, w)
         assert np.array_equal(got_f[k].view(np.uint32), pack_frame(px, ld).numpy().view(np.uint32))
         assert np.array_equal(got_s[k], st.numpy())
+
+
+def _bcast_worker(rank, world, port, q):
+    sys.path.insert(0, str(ROOT))
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    import torch.distributed as dist
+
+    import paper_2409_08669_b200 as ab
+    from paper_2409_08669_b200.views import broadcast_scene
+
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        src = None
+        if rank == 0:
+            a = ab.synthetic_arrays(5, 300, ab.SyntheticSpec(), sh_degree=2, float32=True)
+            src = ab.DeviceScene.from_arrays(a, 2, "cpu", torch.float32)
+        ds = broadcast_scene(src, 300, 2, "cpu", torch.float32)
+        q.put((rank, [t.numpy().copy() for t in (ds.centers, ds.scales, ds.rotations, ds.opacities, ds.sh)]))
+    finally:
+        dist.destroy_process_group()
+
+
+def test_broadcast_scene_gloo_world2():
+    """Rank 0's scene arrives bit-identical on rank 1 (load once,
+    broadcast)."""
+    import paper_2409_08669_b200 as ab
+
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_bcast_worker, args=(r, 2, port, q)) for r in range(2)]
+    for pr in procs:
+        pr.start()
+    got = dict(q.get(timeout=120) for _ in range(2))
+    for pr in procs:
+        pr.join(timeout=60)
+        assert pr.exitcode == 0
+    a = ab.synthetic_arrays(5, 300, ab.SyntheticSpec(), sh_degree=2, float32=True)
+    want = [np.asarray(x, dtype=np.float32) for x in (a.centers, a.scales, a.rotations, a.opacities, a.sh)]
+    for r in (0, 1):
+        for g, w in zip(got[r], want):
+            assert g.shape == w.shape and np.array_equal(g.view(np.uint32), w.view(np.uint32))
