@@ -383,8 +383,19 @@ k_emit_balanced(const uint2* __restrict__ rect, const uint32_t* __restrict__ ord
 // positions of the current interval and keeps the one gap where the ids cross
 // t), so the whole pass reads ~(T + 1) * 32 * log32(P) ids instead of P.
 // ranges[t] = (lb(t), lb(t + 1)); lb(T) = P closes the last tile.
+// tile id of sorted position q: the sorted tile array, or the high word of
+// the exported reference key (the last sort pass then skips the tile copy)
 template <typename TileT>
-__global__ void __launch_bounds__(256) k_ranges_search(const TileT* __restrict__ tiles, const int64_t* __restrict__ d_p,
+struct TileIds {
+    const TileT* tiles;
+    const uint64_t* keys;
+    __device__ __forceinline__ int64_t operator[](int64_t q) const {
+        return keys ? (int64_t)(keys[q] >> 32) : (int64_t)tiles[q];
+    }
+};
+
+template <typename TileT>
+__global__ void __launch_bounds__(256) k_ranges_search(TileIds<TileT> tiles, const int64_t* __restrict__ d_p,
                                                        int64_t n_tiles, int64_t* __restrict__ ranges) {
     const int lane = threadIdx.x & 31;
     const int64_t t = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
@@ -394,14 +405,14 @@ __global__ void __launch_bounds__(256) k_ranges_search(const TileT* __restrict__
     while (hi - lo > 32) {
         const int64_t step = (hi - lo + 31) / 32;
         const int64_t q = lo + lane * step;
-        const bool below = q < hi && (int64_t)tiles[q] < t;
+        const bool below = q < hi && tiles[q] < t;
         const int c = __popc(__ballot_sync(kFull, below));
         const int64_t nlo = c > 0 ? lo + (int64_t)(c - 1) * step + 1 : lo;
         const int64_t qc = lo + (int64_t)c * step;
         hi = (c < 32 && qc < hi) ? qc : hi;
         lo = nlo;
     }
-    const bool below = lo + lane < hi && (int64_t)tiles[lo + lane] < t;
+    const bool below = lo + lane < hi && tiles[lo + lane] < t;
     const int64_t lb = lo + __popc(__ballot_sync(kFull, below));
     if (lane == 0) {
         if (t < n_tiles) ranges[2 * t] = lb;
@@ -476,13 +487,14 @@ static int32_t frame_binning_t(const FrameBinning& fb, cudaStream_t st) {
     tx.mode = 1;
     tx.exp_depth = fb.proj.d_depth;
     tx.exp_keys = fb.keys;
+    tx.skip_keys_out = fb.keys != nullptr;
     rc = radix_sort<TileT, uint32_t>(tiles, gs, stiles, reinterpret_cast<uint32_t*>(fb.gidx), ctr + 3, cap, tbits,
                                      rs2, radix_scratch_bytes<TileT, uint32_t>(cap), st, tx);
     if (rc) return rc;
     if (fb.ev_after_sort) ADR_CUDA_TRY(cudaEventRecord(fb.ev_after_sort, st));
     // (f) tile ranges
-    k_ranges_search<TileT><<<ceil_div((fb.n_tiles + 1) * 32, 256), 256, 0, st>>>(stiles, ctr + 3, fb.n_tiles,
-                                                                                  fb.ranges);
+    k_ranges_search<TileT><<<ceil_div((fb.n_tiles + 1) * 32, 256), 256, 0, st>>>(
+        TileIds<TileT>{stiles, fb.keys}, ctr + 3, fb.n_tiles, fb.ranges);
     ADR_LAUNCH_CHECK();
     if (fb.ev_after_ranges) ADR_CUDA_TRY(cudaEventRecord(fb.ev_after_ranges, st));
     return ADR_OK;

@@ -127,6 +127,7 @@ struct SortExtra {
     int mode = 0;
     const float* exp_depth = nullptr;
     uint64_t* exp_keys = nullptr;
+    bool skip_keys_out = false;   // MODE 1: the exported keys carry the tile ids, no separate copy
     const uint2* gsrc = nullptr;
     uint2* gdst = nullptr;
 };
@@ -218,7 +219,7 @@ radix_downsweep(const K* __restrict__ keys_in, const V* __restrict__ vals_in, K*
             vals_out[g] = val;
             ex.gdst[g] = ex.gsrc[val];
         } else {
-            keys_out[g] = key;
+            if (MODE != 1 || !ex.skip_keys_out) keys_out[g] = key;
             vals_out[g] = val;
             if (MODE == 1 && ex.exp_keys)
                 ex.exp_keys[g] = ((uint64_t)key << 32) | __float_as_uint(ex.exp_depth[val]);
