@@ -396,8 +396,15 @@ struct TileIds {
 
 template <typename TileT>
 __global__ void __launch_bounds__(256) k_ranges_search(TileIds<TileT> tiles, const int64_t* __restrict__ d_p,
-                                                       int64_t n_tiles, int64_t* __restrict__ ranges) {
+                                                       int64_t n_tiles, int64_t* __restrict__ ranges,
+                                                       adr_load_stats* stats) {
     const int lane = threadIdx.x & 31;
+    if (stats && blockIdx.x == 0 && threadIdx.x == 0) {   // the render's load-statistics accumulators
+        stats->sum = 0;
+        stats->sum_sq = 0;
+        stats->min = INT_MAX;
+        stats->max = INT_MIN;
+    }
     const int64_t t = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
     if (t > n_tiles) return;
     const int64_t p = *d_p;
@@ -494,7 +501,7 @@ static int32_t frame_binning_t(const FrameBinning& fb, cudaStream_t st) {
     if (fb.ev_after_sort) ADR_CUDA_TRY(cudaEventRecord(fb.ev_after_sort, st));
     // (f) tile ranges
     k_ranges_search<TileT><<<ceil_div((fb.n_tiles + 1) * 32, 256), 256, 0, st>>>(
-        TileIds<TileT>{stiles, fb.keys}, ctr + 3, fb.n_tiles, fb.ranges);
+        TileIds<TileT>{stiles, fb.keys}, ctr + 3, fb.n_tiles, fb.ranges, fb.stats);
     ADR_LAUNCH_CHECK();
     if (fb.ev_after_ranges) ADR_CUDA_TRY(cudaEventRecord(fb.ev_after_ranges, st));
     return ADR_OK;

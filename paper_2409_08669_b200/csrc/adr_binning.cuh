@@ -34,6 +34,7 @@ struct FrameBinning {
     uint64_t* keys = nullptr;   // optional out: sorted keys (tile << 32 | depth bits)
     int32_t* gidx = nullptr;    // out: sorted Gaussian indices (render record index)
     int64_t* counters = nullptr;
+    adr_load_stats* stats = nullptr;  // optional: reset by the ranges pass (saves the render's init launch)
     void* scratch = nullptr;
     size_t scratch_bytes = 0;
     cudaEvent_t ev_after_scan = nullptr, ev_after_dup = nullptr, ev_after_sort = nullptr,

@@ -175,6 +175,7 @@ int32_t adr_render_frame(const adr_scene* scene, const adr_camera* cam, int32_t 
         fb.keys = buf->d_keys;
         fb.gidx = buf->d_gidx;
         fb.counters = buf->d_counters;
+        fb.stats = buf->d_hist ? nullptr : buf->d_stats;   // with a histogram the init kernel runs
         fb.scratch = L.binning;
         fb.scratch_bytes = L.binning_bytes;
         fb.ev_after_scan = ev[2];
@@ -189,8 +190,10 @@ int32_t adr_render_frame(const adr_scene* scene, const adr_camera* cam, int32_t 
             if (ev[i]) ADR_CUDA_TRY(cudaEventRecord(ev[i], st));
     }
 
-    rc = launch_init_stats(buf->d_stats, buf->d_hist, buf->hist_bins, st);
-    if (rc) return rc;
+    if (n <= 0 || buf->d_hist) {
+        rc = launch_init_stats(buf->d_stats, buf->d_hist, buf->hist_bins, st);
+        if (rc) return rc;
+    }
     RenderArgs ra;
     ra.rec = L.rec;
     ra.idx = reinterpret_cast<const uint32_t*>(buf->d_gidx);
