@@ -275,7 +275,7 @@ int32_t radix_sort(const K* keys_in, const V* vals_in, K* keys_out, V* vals_out,
     const V* src_v = vals_in;
     int bit = 0;
     for (int p = 0; p < passes; ++p) {
-        const int bits = (end_bit - bit + (passes - p) - 1) / (passes - p);  // near-equal split
+        const int bits = (end_bit - bit) / (passes - p);  // near-equal split, wider digits last
         const bool to_out = ((passes - 1 - p) % 2) == 0;
         const bool last = p == passes - 1;
         K* dst_k = to_out ? keys_out : alt_k;
