@@ -207,102 +207,61 @@ int32_t stage_ranges(const uint64_t* keys, int64_t p, int64_t n_tiles, int64_t* 
 
 namespace {
 
-#ifndef ADR_LB_IPT
-#define ADR_LB_IPT 8
-#endif
-constexpr int kLbBlock = 256, kLbIpt = ADR_LB_IPT, kLbTile = kLbBlock * kLbIpt;
-static_assert(kLbIpt % 4 == 0, "vector runs of 4 ranks");
 
-// Generic single-pass exclusive scan with decoupled look-back; Op supplies
-// load(i) -> u64, store(i, exclusive, value) and total(sum).
-template <class Op>
-__global__ void __launch_bounds__(kLbBlock)
-k_scan_lookback(Op op, const int64_t* d_n, int64_t n_static, uint64_t* status, unsigned long long* counter) {
-    __shared__ int64_t sbid;
-    __shared__ uint64_t sred[33];
-    __shared__ uint64_t sexcl;
-    const int64_t n = d_n ? *d_n : n_static;
-    const int64_t bid = dynamic_block_id(counter, &sbid);
-    const int64_t base = bid * kLbTile + (int64_t)threadIdx.x * kLbIpt;
-    uint64_t v[kLbIpt];
-    uint64_t s = 0;
-    const bool full = base + kLbIpt <= n;
-    if (full) {
-        op.load_run(base, v);   // the thread's kLbIpt consecutive items, vector loads
-    } else {
+
+// Pair offsets in rank order without a separate offsets array: the stream
+// is cut into chunks of 256 ranks (one emission block each); this pass sums
+// each chunk's rect areas, k_chunk_scan turns the sums into chunk offsets and
+// P, and the emission block scans its own 256 areas.
+__global__ void __launch_bounds__(256) k_chunk_area_sums(const uint2* __restrict__ rect, const int64_t* __restrict__ d_m,
+                                                         int64_t nc, uint64_t* __restrict__ csum) {
+    // warp per 256-rank chunk, 8 consecutive ranks per lane (four 16-byte loads)
+    const int64_t chunk = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    if (chunk >= nc) return;
+    const int64_t m = *d_m;
+    const int64_t r0 = chunk * 256 + (int64_t)(threadIdx.x & 31) * 8;
+    uint64_t a = 0;
+    if (r0 + 8 <= m) {
+        const uint4* q = reinterpret_cast<const uint4*>(rect + r0);
 #pragma unroll
-        for (int k = 0; k < kLbIpt; ++k) v[k] = base + k < n ? op.load(base + k) : 0ull;
-    }
-#pragma unroll
-    for (int k = 0; k < kLbIpt; ++k) s += v[k];
-    uint64_t btot;
-    const uint64_t tpre = block_exclusive_sum<uint64_t, kLbBlock>(s, sred, &btot);
-    if (threadIdx.x < 32) {
-        const uint64_t e = lookback(status, bid, btot);
-        if (threadIdx.x == 0) sexcl = e;
-    }
-    __syncthreads();
-    uint64_t run = sexcl + tpre;
-    if (full) {
-        uint64_t ex[kLbIpt];
-#pragma unroll
-        for (int k = 0; k < kLbIpt; ++k) {
-            ex[k] = run;
-            run += v[k];
+        for (int k = 0; k < 4; ++k) {
+            const uint4 t = q[k];
+            a += (uint64_t)((t.x >> 16) - (t.x & 0xffffu)) * ((t.y >> 16) - (t.y & 0xffffu));
+            a += (uint64_t)((t.z >> 16) - (t.z & 0xffffu)) * ((t.w >> 16) - (t.w & 0xffffu));
         }
-        op.store_run(base, ex);
     } else {
-#pragma unroll
-        for (int k = 0; k < kLbIpt; ++k) {
-            if (base + k < n) op.store(base + k, run, v[k]);
-            run += v[k];
+        for (int64_t r = r0; r < r0 + 8 && r < m; ++r) {
+            const uint2 inf = rect[r];
+            a += (uint64_t)((inf.x >> 16) - (inf.x & 0xffffu)) * ((inf.y >> 16) - (inf.y & 0xffffu));
         }
     }
-    if (bid == (int64_t)gridDim.x - 1 && threadIdx.x == kLbBlock - 1) op.total(run);
+    a = warp_sum(a);
+    if ((threadIdx.x & 31) == 0) csum[chunk] = a;
 }
 
-// Pair offsets in rank order: off[r] = sum_{r' < r} count(r'), where
-// count(r) is the area of rect[r]'s tile rectangle; clamped to the pair
-// capacity, and off[M] = min(P, cap) closes the table.
-struct RankOffsetsOp {
-    const uint2* rect;
-    uint32_t* off;
-    const int64_t* d_m;
-    int64_t* d_p;        // true pair count
-    int64_t* d_pc;       // pair count clamped to capacity
-    int64_t cap;
-    __device__ uint64_t load(int64_t r) const {
-        const uint2 inf = rect[r];
-        return (uint64_t)((inf.x >> 16) - (inf.x & 0xffffu)) * ((inf.y >> 16) - (inf.y & 0xffffu));
-    }
-    __device__ void store(int64_t r, uint64_t ex, uint64_t) const {
-        off[r] = ex < (uint64_t)cap ? (uint32_t)ex : (uint32_t)cap;
-    }
-    // kLbIpt consecutive ranks starting at a multiple of kLbIpt: 16-byte loads
-    __device__ void load_run(int64_t r, uint64_t* v) const {
-        const uint4* q = reinterpret_cast<const uint4*>(rect + r);
-#pragma unroll
-        for (int k = 0; k < kLbIpt / 2; ++k) {
-            const uint4 t = q[k];
-            v[2 * k] = (uint64_t)((t.x >> 16) - (t.x & 0xffffu)) * ((t.y >> 16) - (t.y & 0xffffu));
-            v[2 * k + 1] = (uint64_t)((t.z >> 16) - (t.z & 0xffffu)) * ((t.w >> 16) - (t.w & 0xffffu));
+// Exclusive scan of the chunk sums in place (one block); P and P clamped to
+// the pair capacity go to the counters.
+__global__ void __launch_bounds__(1024) k_chunk_scan(uint64_t* __restrict__ csum, int64_t nc, int64_t* __restrict__ d_p,
+                                                     int64_t* __restrict__ d_pc, int64_t cap) {
+    __shared__ uint64_t sred[33];
+    const int64_t per = (nc + 1023) / 1024, c0 = (int64_t)threadIdx.x * per;
+    uint64_t s = 0;
+#pragma unroll 8
+    for (int64_t k = 0; k < per; ++k) s += c0 + k < nc ? csum[c0 + k] : 0ull;
+    uint64_t tot;
+    uint64_t run = block_exclusive_sum<uint64_t, 1024>(s, sred, &tot);
+    for (int64_t k = 0; k < per; ++k) {
+        if (c0 + k < nc) {
+            const uint64_t v = csum[c0 + k];
+            csum[c0 + k] = run;
+            run += v;
         }
     }
-    __device__ void store_run(int64_t r, const uint64_t* ex) const {
-        uint32_t c[kLbIpt];
-#pragma unroll
-        for (int k = 0; k < kLbIpt; ++k) c[k] = ex[k] < (uint64_t)cap ? (uint32_t)ex[k] : (uint32_t)cap;
-        uint4* q = reinterpret_cast<uint4*>(off + r);
-#pragma unroll
-        for (int k = 0; k < kLbIpt / 4; ++k) q[k] = make_uint4(c[4 * k], c[4 * k + 1], c[4 * k + 2], c[4 * k + 3]);
+    if (threadIdx.x == 0) {
+        *d_p = (int64_t)tot;
+        *d_pc = tot < (uint64_t)cap ? (int64_t)tot : cap;
     }
-    __device__ void total(uint64_t t) const {
-        const int64_t pc = t < (uint64_t)cap ? (int64_t)t : cap;
-        *d_p = (int64_t)t;
-        *d_pc = pc;
-        off[*d_m] = (uint32_t)pc;
-    }
-};
+}
 
 // ---- rank-ordered pair stream ---------------------------------------------
 // Rank r owns stream positions [off[r], off[r+1]), row-major over its tile
@@ -317,22 +276,27 @@ struct RankOffsetsOp {
 // start offsets, so lanes do equal work however uneven the rectangles are.
 template <typename TileT>
 __global__ void __launch_bounds__(256)
-k_emit_balanced(const uint2* __restrict__ rect, const uint32_t* __restrict__ order, const uint32_t* __restrict__ off,
+k_emit_balanced(const uint2* __restrict__ rect, const uint32_t* __restrict__ order, const uint64_t* __restrict__ coff,
                 const int64_t* __restrict__ d_m,
                 const int64_t* __restrict__ d_pc, int32_t tiles_x, TileT* __restrict__ tiles, uint32_t* __restrict__ gs) {
+    __shared__ uint64_t sred[33];
     const int lane = threadIdx.x & 31;
     const uint32_t m = (uint32_t)*d_m;
     const uint32_t pc = (uint32_t)*d_pc;
-    const uint32_t r0 = (uint32_t)(((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5) * 32u;
-    if (r0 >= m) return;
-    const uint32_t r = r0 + lane;
+    const uint32_t r = blockIdx.x * 256u + threadIdx.x;   // the block is one 256-rank chunk
+    const uint32_t r0 = r - (uint32_t)lane;
     const bool valid = r < m;
     const uint2 inf = valid ? rect[r] : make_uint2(0, 0);
     const uint32_t gidx = valid ? order[r] : 0u;
-    const uint32_t o = valid ? off[r] : pc;
+    // this rank's stream offset: chunk offset + exclusive scan of the chunk's areas
+    const uint64_t area = (uint64_t)((inf.x >> 16) - (inf.x & 0xffffu)) * ((inf.y >> 16) - (inf.y & 0xffffu));
+    uint64_t btot;
+    const uint64_t g64 = coff[blockIdx.x] + block_exclusive_sum<uint64_t, 256>(area, sred, &btot);
+    if (r0 >= m) return;
+    const uint32_t o = valid ? (g64 < pc ? (uint32_t)g64 : pc) : pc;
     const uint32_t wstart = __shfl_sync(kFull, o, 0);
-    uint32_t wend = r0 + 32 < m ? off[r0 + 32] : pc;
-    wend = wend < pc ? wend : pc;
+    const uint64_t wend64 = __shfl_sync(kFull, g64 + area, 31);   // invalid lanes have area 0
+    const uint32_t wend = wend64 < pc ? (uint32_t)wend64 : pc;
     const uint32_t x0 = inf.x & 0xffffu, w = (inf.x >> 16) - x0, y0 = inf.y & 0xffffu;
     const float rw = w ? __frcp_rn((float)w) : 0.0f;
     const uint32_t xy0 = x0 | (y0 << 16);
@@ -430,14 +394,14 @@ __global__ void __launch_bounds__(256) k_ranges_search(TileIds<TileT> tiles, con
 }  // namespace
 
 size_t frame_binning_scratch(int64_t n, int64_t cap, int64_t n_tiles) {
-    const int64_t nlb = ceil_div(n > 0 ? n : 1, kLbTile);
+    const int64_t nc = ceil_div(n > 0 ? n : 1, 256);
     const bool wide = n_tiles > 65536;
     const size_t tile_sz = wide ? 4 : 2;
     size_t s = 0;
-    s += align_up(4 * (size_t)n) + align_up(4 * (size_t)(n + 1));      // skey, off
+    s += align_up(4 * (size_t)n);                                      // skey
+    s += align_up(8 * (size_t)nc);                                     // chunk offsets
     s += align_up(8 * (size_t)n);                                      // rect by rank
     s += radix_scratch_bytes<uint32_t, uint32_t>(n);
-    s += lookback_bytes(nlb);
     s += 2 * align_up(tile_sz * (size_t)cap) + align_up(4 * (size_t)cap);  // tiles, sorted tiles, gs
     s += wide ? radix_scratch_bytes<uint32_t, uint32_t>(cap) : radix_scratch_bytes<uint16_t, uint32_t>(cap);
     return s + 8192;
@@ -448,11 +412,9 @@ static int32_t frame_binning_t(const FrameBinning& fb, cudaStream_t st) {
     Carver c(fb.scratch, fb.scratch_bytes);
     const int64_t n = fb.n, cap = fb.cap;
     uint32_t* skey = c.take<uint32_t>(n);
-    uint32_t* off = c.take<uint32_t>(n + 1);
+    uint64_t* coff = c.take<uint64_t>(ceil_div(n, 256));
     uint2* rect = c.take<uint2>(n);
     void* rs1 = c.take<char>((int64_t)radix_scratch_bytes<uint32_t, uint32_t>(n));
-    const int64_t nlb = ceil_div(n, kLbTile);
-    uint64_t* st2 = c.take<uint64_t>(nlb + 1);
     TileT* tiles = c.take<TileT>(cap);
     TileT* stiles = c.take<TileT>(cap);
     uint32_t* gs = c.take<uint32_t>(cap);
@@ -472,19 +434,18 @@ static int32_t frame_binning_t(const FrameBinning& fb, cudaStream_t st) {
     int32_t rc = radix_sort<uint32_t, uint32_t>(fb.dkey, nullptr, skey, fb.order, nullptr, n, 32, rs1,
                                                 radix_scratch_bytes<uint32_t, uint32_t>(n), st, dx);
     if (rc) return rc;
-    // (c) pair offsets in rank order, and P
-    ADR_CUDA_TRY(cudaMemsetAsync(st2, 0, sizeof(uint64_t) * (nlb + 1), st));
-    RankOffsetsOp oo{rect, off, ctr + 2, ctr + 0, ctr + 3, cap};
-    k_scan_lookback<RankOffsetsOp><<<nlb, kLbBlock, 0, st>>>(oo, ctr + 2, n, st2,
-                                                            reinterpret_cast<unsigned long long*>(st2 + nlb));
+    // (c) pair offsets in rank order (per 256-rank chunk), and P
+    const int64_t nc = ceil_div(n, 256);
+    k_chunk_area_sums<<<ceil_div(nc * 32, 256), 256, 0, st>>>(rect, ctr + 2, nc, coff);
+    ADR_LAUNCH_CHECK();
+    k_chunk_scan<<<1, 1024, 0, st>>>(coff, nc, ctr + 0, ctr + 3, cap);
     ADR_LAUNCH_CHECK();
     if (fb.ev_after_scan) ADR_CUDA_TRY(cudaEventRecord(fb.ev_after_scan, st));
     // (d) emission of the stream as (tile, Gaussian)
     int tbits = 0;
     while ((int64_t(1) << tbits) < fb.n_tiles) ++tbits;
     if (tbits == 0) tbits = 1;
-    k_emit_balanced<TileT><<<ceil_div(n, 256), 256, 0, st>>>(rect, fb.order, off, ctr + 2, ctr + 3, fb.tiles_x,
-                                                              tiles, gs);
+    k_emit_balanced<TileT><<<nc, 256, 0, st>>>(rect, fb.order, coff, ctr + 2, ctr + 3, fb.tiles_x, tiles, gs);
     ADR_LAUNCH_CHECK();
     if (fb.ev_after_dup) ADR_CUDA_TRY(cudaEventRecord(fb.ev_after_dup, st));
     // (e) stable radix sort by tile id; the last pass writes the sorted
