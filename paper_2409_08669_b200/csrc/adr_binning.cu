@@ -243,19 +243,25 @@ __global__ void __launch_bounds__(256) k_chunk_area_sums(const uint2* __restrict
 // the pair capacity go to the counters.
 __global__ void __launch_bounds__(1024) k_chunk_scan(uint64_t* __restrict__ csum, int64_t nc, int64_t* __restrict__ d_p,
                                                      int64_t* __restrict__ d_pc, int64_t cap) {
+    // warp w owns the contiguous segment [w*seg, (w+1)*seg), read in coalesced
+    // rounds of 32: pass 1 sums it, a block scan of the 32 warp sums gives each
+    // segment's start, pass 2 (L1-resident re-read) writes the prefixes
     __shared__ uint64_t sred[33];
-    const int64_t per = (nc + 1023) / 1024, c0 = (int64_t)threadIdx.x * per;
-    uint64_t s = 0;
-#pragma unroll 8
-    for (int64_t k = 0; k < per; ++k) s += c0 + k < nc ? csum[c0 + k] : 0ull;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int64_t seg = (nc + 31) / 32, s0 = (int64_t)warp * seg;
+    const int64_t s1 = s0 + seg < nc ? s0 + seg : nc;
+    uint64_t sum = 0;
+    for (int64_t i = s0 + lane; i < s1; i += 32) sum += csum[i];
+    sum = warp_sum(sum);
     uint64_t tot;
-    uint64_t run = block_exclusive_sum<uint64_t, 1024>(s, sred, &tot);
-    for (int64_t k = 0; k < per; ++k) {
-        if (c0 + k < nc) {
-            const uint64_t v = csum[c0 + k];
-            csum[c0 + k] = run;
-            run += v;
-        }
+    uint64_t run = block_exclusive_sum<uint64_t, 1024>(lane == 0 ? sum : 0ull, sred, &tot);
+    run = __shfl_sync(kFull, run, 0);
+    for (int64_t base = s0; base < s1; base += 32) {
+        const int64_t i = base + lane;
+        const uint64_t v = i < s1 ? csum[i] : 0ull;
+        const uint64_t inc = warp_inclusive_sum(v);
+        if (i < s1) csum[i] = run + inc - v;
+        run += __shfl_sync(kFull, inc, 31);
     }
     if (threadIdx.x == 0) {
         *d_p = (int64_t)tot;
