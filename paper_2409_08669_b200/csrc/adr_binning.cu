@@ -286,6 +286,7 @@ k_emit_balanced(const uint2* __restrict__ rect, const uint32_t* __restrict__ ord
                 const int64_t* __restrict__ d_m,
                 const int64_t* __restrict__ d_pc, int32_t tiles_x, TileT* __restrict__ tiles, uint32_t* __restrict__ gs) {
     __shared__ uint64_t sred[33];
+    __shared__ uint32_t sred32[33];
     const int lane = threadIdx.x & 31;
     const uint32_t m = (uint32_t)*d_m;
     const uint32_t pc = (uint32_t)*d_pc;
@@ -296,8 +297,14 @@ k_emit_balanced(const uint2* __restrict__ rect, const uint32_t* __restrict__ ord
     const uint32_t gidx = valid ? order[r] : 0u;
     // this rank's stream offset: chunk offset + exclusive scan of the chunk's areas
     const uint64_t area = (uint64_t)((inf.x >> 16) - (inf.x & 0xffffu)) * ((inf.y >> 16) - (inf.y & 0xffffu));
-    uint64_t btot;
-    const uint64_t g64 = coff[blockIdx.x] + block_exclusive_sum<uint64_t, 256>(area, sred, &btot);
+    uint64_t g64;
+    if constexpr (sizeof(TileT) == 2) {   // areas <= 2^16 tiles, a chunk's sum < 2^24: 32-bit scan
+        uint32_t btot;
+        g64 = coff[blockIdx.x] + block_exclusive_sum<uint32_t, 256>((uint32_t)area, sred32, &btot);
+    } else {
+        uint64_t btot;
+        g64 = coff[blockIdx.x] + block_exclusive_sum<uint64_t, 256>(area, sred, &btot);
+    }
     if (r0 >= m) return;
     const uint32_t o = valid ? (g64 < pc ? (uint32_t)g64 : pc) : pc;
     const uint32_t wstart = __shfl_sync(kFull, o, 0);
