@@ -217,7 +217,7 @@ radix_downsweep(const K* __restrict__ keys_in, const V* __restrict__ vals_in, K*
         const int64_t g = goff[digit_of(key, bit, R - 1)] + i;
         if (MODE == 2) {
             vals_out[g] = val;
-            ex.gdst[g] = ex.gsrc[val];
+            ex.gdst[g] = __ldg(ex.gsrc + val);
         } else {
             if (MODE != 1 || !ex.skip_keys_out) keys_out[g] = key;
             vals_out[g] = val;
