@@ -222,7 +222,7 @@ radix_downsweep(const K* __restrict__ keys_in, const V* __restrict__ vals_in, K*
             if (MODE != 1 || !ex.skip_keys_out) keys_out[g] = key;
             vals_out[g] = val;
             if (MODE == 1 && ex.exp_keys)
-                ex.exp_keys[g] = ((uint64_t)key << 32) | __float_as_uint(ex.exp_depth[val]);
+                ex.exp_keys[g] = ((uint64_t)key << 32) | __float_as_uint(__ldcg(ex.exp_depth + val));
         }
     }
 }
