@@ -208,7 +208,11 @@ typedef struct {
     uint64_t* d_keys;             /* (pair_capacity,) sorted keys, optional */
     int32_t* d_gidx;              /* (pair_capacity,) sorted Gaussian indices (required) */
     int64_t* d_ranges;            /* (n_tiles,2)                           */
-    int64_t* d_counters;          /* [0]=P, [1]=culled, [2]=M (Gaussians with pairs) */
+    int64_t* d_counters;          /* 8 entries: [0]=P, [1]=culled, [2]=M (Gaussians with
+                                     pairs), [3]=min(P, capacity), [4]=valid rows with a NaN
+                                     colour, [5]=ceil-ambiguous culling extents (log fence:
+                                     0 proves the extents equal numpy's), [6]=1 when
+                                     P > pair_capacity (frame truncated, re-run larger) */
     adr_load_stats* d_stats;
     int32_t* d_hist;              /* optional, hist_bins entries           */
     int32_t hist_bins;

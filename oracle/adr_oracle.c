@@ -18,6 +18,29 @@
 #endif
 
 #define TILE 16
+#define PAIR_CHUNK 2048 /* render.py:36 _PAIR_CHUNK: the blend's frozen-break granularity */
+
+/* numpy's float64 -> int32 astype on x86 (cvttsd2si): out-of-range and NaN
+ * give INT32_MIN ("integer indefinite"), projection.py:419-420. */
+static inline int32_t np_i32(double v) {
+    return (v >= -2147483648.0 && v < 2147483648.0) ? (int32_t)v : INT32_MIN;
+}
+
+/* Culling extents are ceil(min(sqrt(2 s log_ratio), r_o)) (projection.py:
+ * 387-396).  numpy's fp64 log and orc_log are both faithfully rounded, so
+ * they differ by at most 2 ulp; that moves the sqrt by far less than
+ * v * 2^-48.  An extent is "ceil-ambiguous" when the sqrt that min() can
+ * select lies within that margin of a positive integer: only then can the
+ * log's last bit change the output.  The count proves per frame that it
+ * does not. */
+int32_t orc_ceil_ambiguous(double v, double r_o) {
+    if (!(v == v) || v > r_o * (1.0 + 0x1p-46) + 1e-300) return 0;
+    const double m = nearbyint(v);
+    return m >= 1.0 && fabs(v - m) <= v * 0x1p-48;
+}
+
+static int64_t g_ambiguous = 0;
+int64_t orc_preprocess_ambiguous(void) { return g_ambiguous; }
 
 /* ------------------------------------------------------------------------ */
 /* numpy float32 exp (render.py:96 calls np.exp on f32). */
@@ -235,13 +258,23 @@ static void project_row(int64_t i, int32_t deg, const double* centers, const dou
     } else {
         alive = alive && (sigma > alpha_low);
         const double log_ratio = orc_log(np_max(sigma / alpha_low, 1e-300));
+        int32_t amb = 0;
         if (mode == ORC_CIRCLE) {
             const double r_ad = sqrt((2.0 * lam_max) * log_ratio);
             ex = ceil(np_min(r_ad, r_o_real));
             ey = ex;
+            amb = orc_ceil_ambiguous(r_ad, r_o_real);
         } else {
-            ex = ceil(np_min(sqrt((2.0 * sxx) * log_ratio), r_o_real));
-            ey = ceil(np_min(sqrt((2.0 * syy) * log_ratio), r_o_real));
+            const double vx = sqrt((2.0 * sxx) * log_ratio), vy = sqrt((2.0 * syy) * log_ratio);
+            ex = ceil(np_min(vx, r_o_real));
+            ey = ceil(np_min(vy, r_o_real));
+            amb = orc_ceil_ambiguous(vx, r_o_real) + orc_ceil_ambiguous(vy, r_o_real);
+        }
+        if (alive && amb) {
+#ifdef _OPENMP
+#pragma omp atomic
+#endif
+            g_ambiguous += amb;
         }
     }
     alive = alive && (ex >= 1.0) && (ey >= 1.0);
@@ -279,8 +312,8 @@ static void project_row(int64_t i, int32_t deg, const double* centers, const dou
     for (int ch = 0; ch < 3; ++ch) color[3 * i + ch] = (float)sh_channel(coeffs, ch, deg, d0, d1, d2);
     opacity_o[i] = (float)sigma;
     lambda_max[i] = (float)lam_max;
-    ext_x[i] = (int32_t)ex;
-    ext_y[i] = (int32_t)ey;
+    ext_x[i] = np_i32(ex);
+    ext_y[i] = np_i32(ey);
 }
 
 void orc_preprocess(int64_t n, int32_t sh_degree, const double* centers, const double* scales,
@@ -289,6 +322,7 @@ void orc_preprocess(int64_t n, int32_t sh_degree, const double* centers, const d
                     uint8_t* valid, float* mean2d, float* cov2d, float* conic, float* depth,
                     float* color, float* opacity, float* lambda_max, int32_t* ext_x,
                     int32_t* ext_y, int32_t nthreads) {
+    g_ambiguous = 0;
 #ifdef _OPENMP
 #pragma omp parallel for schedule(static) num_threads(nthreads > 0 ? nthreads : 1)
 #endif
@@ -400,7 +434,26 @@ int32_t orc_identify_tile_ranges(int64_t p, const uint64_t* sorted_keys, int64_t
 }
 
 /* render.py:57-125 restated per pixel as the scalar recurrence the chunked
- * numpy kernel reproduces, and render.py:128-171. */
+ * numpy kernel reproduces, and render.py:128-171.
+ *
+ * Per pixel, pair k of the tile's span (render.py:89-120):
+ *   eff   = alpha >= alpha_low ? alpha : 0          (:96-97; NaN alpha -> 0)
+ *   live  = T_before >= term                        (:104)
+ *   C    += live ? (eff * T_before) * colour : 0    (:105-108)
+ *   count+= live && eff > 0                         (:109)
+ *   T     = T_before * (1 - eff)                    (:102, cumprod)
+ *   the pixel freezes right after the first pair with T < term (:113-120).
+ * With term <= 1 only contributing pairs change T, so this is the familiar
+ * "composite, then stop once T < term".  With term > 1 no pair is ever live
+ * and every pixel freezes at the span's first pair with T = 1 - eff(first);
+ * with a NaN term nothing is live and nothing freezes.
+ *
+ * NaN colours (NaN SH coefficients pass np.clip, projection.py:163): the
+ * reference adds weight * colour for EVERY pair of every processed chunk,
+ * frozen or not, and 0 * NaN = NaN, so a NaN colour channel among the pairs
+ * of the chunks the tile processes — up to the end of the 2048-pair chunk in
+ * which its last pixel froze (frozen.all() break, :119-120), else the whole
+ * span — turns that channel NaN for every pixel of the tile. */
 void orc_render(int32_t width, int32_t height, int32_t tiles_x, int32_t tiles_y,
                 const float* mean2d, const float* conic, const float* opacity,
                 const float* color, const int64_t* gidx, const int64_t* ranges,
@@ -420,10 +473,13 @@ void orc_render(int32_t width, int32_t height, int32_t tiles_x, int32_t tiles_y,
         const int32_t x1 = x0 + TILE < width ? x0 + TILE : width;
         const int32_t y1 = y0 + TILE < height ? y0 + TILE : height;
         const int64_t start = ranges[2 * tile], end = ranges[2 * tile + 1];
+        int all_frozen = 1;
+        int64_t last_freeze = -1;
         for (int32_t py = y0; py < y1; ++py)
             for (int32_t px = x0; px < x1; ++px) {
                 float T = 1.0f, C0 = 0.0f, C1 = 0.0f, C2 = 0.0f;
                 int32_t cnt = 0;
+                int64_t froze = -1;
                 const float fpx = (float)px, fpy = (float)py;
                 for (int64_t k = start; k < end; ++k) {
                     const int64_t g = gidx[k];
@@ -433,15 +489,22 @@ void orc_render(int32_t width, int32_t height, int32_t tiles_x, int32_t tiles_y,
                     const float power = (-0.5f * ((a * dx) * dx + (c * dy) * dy)) - ((b * dx) * dy);
                     float alpha = opacity[g] * orc_exp_np(power);
                     alpha = (alpha != alpha) ? alpha : (alpha < 0.99f ? alpha : 0.99f);
-                    if (!(alpha >= alpha_low32)) continue;                 /* :97 */
-                    const float wgt = alpha * T;                           /* :104-105 */
-                    C0 = C0 + wgt * color[3 * g];
-                    C1 = C1 + wgt * color[3 * g + 1];
-                    C2 = C2 + wgt * color[3 * g + 2];
-                    T = T * (1.0f - alpha);
-                    ++cnt;
-                    if (T < term32) break;                                 /* :113-120 */
+                    const float eff = alpha >= alpha_low32 ? alpha : 0.0f;   /* :97 */
+                    if (T >= term32 && eff > 0.0f) {                         /* :104-109 */
+                        const float wgt = eff * T;
+                        C0 = C0 + wgt * color[3 * g];
+                        C1 = C1 + wgt * color[3 * g + 1];
+                        C2 = C2 + wgt * color[3 * g + 2];
+                        ++cnt;
+                    }
+                    T = T * (1.0f - eff);
+                    if (T < term32) {                                        /* :113-120 */
+                        froze = k - start;
+                        break;
+                    }
                 }
+                if (froze < 0) all_frozen = 0;
+                else if (froze > last_freeze) last_freeze = froze;
                 float* out = pixels + 3 * ((int64_t)py * width + px);
                 float o0 = C0 + T * background[0], o1 = C1 + T * background[1],
                       o2 = C2 + T * background[2];
@@ -450,6 +513,21 @@ void orc_render(int32_t width, int32_t height, int32_t tiles_x, int32_t tiles_y,
                 out[2] = o2 < 0.0f ? 0.0f : (o2 > 1.0f ? 1.0f : o2);
                 counts[(int64_t)py * width + px] = cnt;
             }
+        /* NaN-colour poisoning over the processed chunks */
+        int64_t processed = end - start;
+        if (all_frozen && last_freeze >= 0) {
+            const int64_t chunk_end = (last_freeze / PAIR_CHUNK + 1) * PAIR_CHUNK;
+            if (chunk_end < processed) processed = chunk_end;
+        }
+        int poison = 0;
+        for (int64_t k = start; k < start + processed; ++k)
+            for (int ch = 0; ch < 3; ++ch)
+                if (color[3 * gidx[k] + ch] != color[3 * gidx[k] + ch]) poison |= 1 << ch;
+        if (poison)
+            for (int32_t py = y0; py < y1; ++py)
+                for (int32_t px = x0; px < x1; ++px)
+                    for (int ch = 0; ch < 3; ++ch)
+                        if (poison >> ch & 1) pixels[3 * ((int64_t)py * width + px) + ch] = NAN;
     }
     (void)tiles_y;
     (void)nthreads;

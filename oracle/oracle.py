@@ -71,6 +71,9 @@ def lib():
         _lib.orc_log.argtypes = [ctypes.c_double]
         _lib.orc_inclusive_sum.restype = ctypes.c_int32
         _lib.orc_identify_tile_ranges.restype = ctypes.c_int32
+        _lib.orc_ceil_ambiguous.restype = ctypes.c_int32
+        _lib.orc_ceil_ambiguous.argtypes = [ctypes.c_double, ctypes.c_double]
+        _lib.orc_preprocess_ambiguous.restype = ctypes.c_int64
     return _lib
 
 
@@ -184,6 +187,9 @@ def preprocess(scene, cam, mode="aabb", alpha_low=1.0 / 255.0, dilation=0.3, thr
             _p(out["valid"]), _p(out["mean2d"]), _p(out["cov2d"]), _p(out["conic"]),
             _p(out["depth"]), _p(out["color"]), _p(out["opacity"]), _p(out["lambda_max"]),
             _p(out["ext_x"]), _p(out["ext_y"]), ctypes.c_int32(threads or os.cpu_count()))
+    # extents whose ceil could flip under a 2-ulp change of the fp64 log
+    # (orc_ceil_ambiguous): 0 proves numpy's log gives the same extents
+    out["ambiguous_extents"] = int(lib().orc_preprocess_ambiguous()) if n else 0
     return out
 
 

@@ -266,6 +266,7 @@ __global__ void __launch_bounds__(1024) k_chunk_scan(uint64_t* __restrict__ csum
     if (threadIdx.x == 0) {
         *d_p = (int64_t)tot;
         *d_pc = tot < (uint64_t)cap ? (int64_t)tot : cap;
+        d_pc[3] = tot > (uint64_t)cap ? 1 : 0;   // counters[6]: frame truncated
     }
 }
 

@@ -154,6 +154,8 @@ int32_t adr_render_frame(const adr_scene* scene, const adr_camera* cam, int32_t 
     fp.dkey = L.dkey;
     fp.d_m = buf->d_counters + 2;
     fp.culled = reinterpret_cast<unsigned long long*>(buf->d_counters + 1);
+    fp.nan_colors = reinterpret_cast<unsigned long long*>(buf->d_counters + 4);
+    fp.ambiguous = reinterpret_cast<unsigned long long*>(buf->d_counters + 5);
     fp.tiles_x = tx;
     fp.tiles_y = ty;
     int32_t rc = launch_preprocess(*scene, *cam, mode, alpha_low, dilation, buf->proj, &fp, st);
@@ -211,6 +213,7 @@ int32_t adr_render_frame(const adr_scene* scene, const adr_camera* cam, int32_t 
     ra.stats = buf->d_stats;
     ra.hist = buf->d_hist;
     ra.hist_bins = buf->hist_bins;
+    ra.nan_flag = buf->d_counters + 4;
     rc = launch_render(ra, st);
     if (rc) return rc;
     if (ev[6]) ADR_CUDA_TRY(cudaEventRecord(ev[6], st));

@@ -76,6 +76,8 @@ struct FusedPre {
     unsigned long long* culled = nullptr;     // += number of !valid rows
     uint32_t* dkey = nullptr;                 // depth-sort key (all-ones: no pairs)
     int64_t* d_m = nullptr;                   // += number of Gaussians with pairs (zeroed)
+    unsigned long long* nan_colors = nullptr; // += valid rows with a NaN colour channel
+    unsigned long long* ambiguous = nullptr;  // += ceil-ambiguous extents (log fence)
     int32_t tiles_x = 0, tiles_y = 0;
 };
 
@@ -97,6 +99,7 @@ struct RenderArgs {
     adr_load_stats* stats;    // may be null
     int32_t* hist;            // may be null
     int32_t hist_bins;
+    const int64_t* nan_flag;  // device count of NaN-colour rows (null: always check poisoning)
 };
 
 int32_t launch_render(const RenderArgs& a, cudaStream_t st);

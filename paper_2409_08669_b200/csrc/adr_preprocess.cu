@@ -68,7 +68,7 @@ __device__ __forceinline__ void stage_sh(const T* __restrict__ sh, int64_t first
     const T* src = sh + first * K3;
     const int total = count * K3;
     if constexpr (sizeof(T) == 4 && K3 % 4 == 0) {
-        if (count == kPreBlock) {
+        if (count == kPreBlock && (reinterpret_cast<uintptr_t>(src) & 15u) == 0) {
             // all K3/4 vector loads of this thread in flight before any store
             constexpr int kVec = K3 / 4;
             const float4* s4 = reinterpret_cast<const float4*>(src);
@@ -122,6 +122,8 @@ k_preprocess(const T* __restrict__ centers, const T* __restrict__ scales,
     bool alive = false;
     bool selected = false;   // fused: touches >= 1 tile
     uint32_t dbits = 0;      // fused: float32 depth bits
+    int ambiguous = 0;       // fused: ceil-ambiguous extents of this row (log fence)
+    bool nan_color = false;  // fused: a valid row with a NaN colour channel
     if (i < n) {
         const double* R = cam.rot;
         const double c0 = (double)ac[0], c1 = (double)ac[1], c2 = (double)ac[2];
@@ -198,11 +200,16 @@ k_preprocess(const T* __restrict__ centers, const T* __restrict__ scales,
             alive = alive && (sigma > alpha_low);
             const double log_ratio = log_fd(np_max(__ddiv_rn(sigma, alpha_low), 1e-300));
             if (mode == ADR_MODE_CIRCLE) {
-                ex = ceil(np_min(__dsqrt_rn(MUL(MUL(2.0, lam_max), log_ratio)), r_o_real));
+                const double v = __dsqrt_rn(MUL(MUL(2.0, lam_max), log_ratio));
+                ex = ceil(np_min(v, r_o_real));
                 ey = ex;
+                if (FUSED && alive) ambiguous = ceil_ambiguous(v, r_o_real);
             } else {
-                ex = ceil(np_min(__dsqrt_rn(MUL(MUL(2.0, sxx), log_ratio)), r_o_real));
-                ey = ceil(np_min(__dsqrt_rn(MUL(MUL(2.0, syy), log_ratio)), r_o_real));
+                const double vx = __dsqrt_rn(MUL(MUL(2.0, sxx), log_ratio));
+                const double vy = __dsqrt_rn(MUL(MUL(2.0, syy), log_ratio));
+                ex = ceil(np_min(vx, r_o_real));
+                ey = ceil(np_min(vy, r_o_real));
+                if (FUSED && alive) ambiguous = ceil_ambiguous(vx, r_o_real) + ceil_ambiguous(vy, r_o_real);
             }
         }
         alive = alive && (ex >= 1.0) && (ey >= 1.0);
@@ -245,10 +252,12 @@ k_preprocess(const T* __restrict__ centers, const T* __restrict__ scales,
             out.d_color[3 * i + 2] = c2f;
             out.d_opacity[i] = op;
             out.d_lambda_max[i] = __double2float_rn(lam_max);
-            out.d_ext_x[i] = (int32_t)ex;
-            out.d_ext_y[i] = (int32_t)ey;
+            const int32_t ix = np_i32(ex), iy = np_i32(ey);
+            out.d_ext_x[i] = ix;
+            out.d_ext_y[i] = iy;
             if (FUSED) {
-                const Rect r = tile_rect(m2.x, m2.y, (int32_t)ex, (int32_t)ey, true, fused.tiles_x, fused.tiles_y);
+                nan_color = c0f != c0f || c1f != c1f || c2f != c2f;
+                const Rect r = tile_rect(m2.x, m2.y, ix, iy, true, fused.tiles_x, fused.tiles_y);
                 selected = r.count() > 0;
                 dbits = __float_as_uint(dz);
                 Record R;
@@ -281,9 +290,15 @@ k_preprocess(const T* __restrict__ centers, const T* __restrict__ scales,
         const int lane = threadIdx.x & 31;
         const uint32_t culled = __ballot_sync(kFull, i < n && !alive);
         const uint32_t sb = __ballot_sync(kFull, selected);
+        const uint32_t nanb = __ballot_sync(kFull, nan_color);
+        if (__any_sync(kFull, ambiguous != 0)) {
+            const int amb = __reduce_add_sync(kFull, (unsigned)ambiguous);
+            if (lane == 0 && fused.ambiguous) atomicAdd(fused.ambiguous, (unsigned long long)amb);
+        }
         if (lane == 0) {
             if (culled) atomicAdd(fused.culled, (unsigned long long)__popc(culled));
             if (sb) atomicAdd(reinterpret_cast<unsigned long long*>(fused.d_m), (unsigned long long)__popc(sb));
+            if (nanb && fused.nan_colors) atomicAdd(fused.nan_colors, (unsigned long long)__popc(nanb));
         }
     }
 }

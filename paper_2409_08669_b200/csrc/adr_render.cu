@@ -36,6 +36,10 @@ struct RecSource {
     const Record* rec;
     const uint32_t* idx;
     __device__ __forceinline__ Record load(int64_t j) const { return rec[idx[j]]; }
+    __device__ __forceinline__ uint32_t nan_bits(int64_t j) const {
+        const float* r = reinterpret_cast<const float*>(rec + idx[j]);
+        return (uint32_t)(r[6] != r[6]) | ((uint32_t)(r[7] != r[7]) << 1) | ((uint32_t)(r[8] != r[8]) << 2);
+    }
 };
 
 // Record source for the stage API: Projection SoA + int64 Gaussian indices.
@@ -60,7 +64,28 @@ struct ProjSource {
         r.c = make_float4(c2, tau, hx, hy);
         return r;
     }
+    __device__ __forceinline__ uint32_t nan_bits(int64_t j) const {
+        const float* c = color + 3 * gidx[j];
+        return (uint32_t)(c[0] != c[0]) | ((uint32_t)(c[1] != c[1]) << 1) | ((uint32_t)(c[2] != c[2]) << 2);
+    }
 };
+
+constexpr int kPairChunk = 2048;   // sb/render.py:36 _PAIR_CHUNK (frozen-break granularity)
+
+// NaN-colour poisoning (sb/render.py:106-108, 119-120): the reference adds
+// weight * colour for EVERY pair of every chunk it processes, frozen pixel or
+// not, and 0 * NaN = NaN, so a NaN colour channel among the pairs
+// [start, processed_end) turns that channel NaN for every pixel of the tile.
+// processed_end is the end of the 2048-pair chunk in which the tile's last
+// pixel froze (frozen.all() break), or the span end.  Returns the 3 channel
+// bits (block-uniform; every thread must call it).
+template <class Src>
+__device__ __forceinline__ uint32_t poison_bits(const Src& src, int64_t start, int64_t processed_end) {
+    uint32_t bits = 0;
+    for (int64_t j = start + threadIdx.x; j < processed_end; j += blockDim.x) bits |= src.nan_bits(j);
+    return (uint32_t)(__syncthreads_or(bits & 1u) != 0) | ((uint32_t)(__syncthreads_or(bits & 2u) != 0) << 1) |
+           ((uint32_t)(__syncthreads_or(bits & 4u) != 0) << 2);
+}
 
 // predicated increment (keeps the counter in place: no select + copy)
 __device__ __forceinline__ void inc_if(int& c, bool p) {
@@ -174,15 +199,18 @@ __device__ __forceinline__ void blend_scalar(float fpx, float fpy, const float4&
     if (T < term) done = true;
 }
 
-// kFlagDone: a pixel's "done" state is an explicit flag.  When the
-// termination threshold is <= 1 it is implied by T itself (T starts at 1, only
+// term_threshold <= 1 (the render path of every frame): a pixel's "done"
+// (frozen) state is implied by T itself — T starts at 1 >= term, only
 // contributing blends change it and the reference tests T < term right after
-// each of them, render.py:110-112), so the flags — and their registers — go.
-template <class Src, bool kFlagDone>
+// each of them (render.py:110-112).  term > 1 or NaN is k_render_unlit below.
+// nan_flag: null = always check NaN-colour poisoning (stage API); otherwise
+// only when *nan_flag != 0 (the fused frame's count of NaN-colour rows).
+template <class Src>
 __global__ void __launch_bounds__(kRenderThreads, Src::kMinBlocks)
 k_render(Src src, const int64_t* __restrict__ ranges, int32_t width, int32_t height, int32_t tiles_x, float bg0,
          float bg1, float bg2, float alpha_low, float term, float* __restrict__ pixels, int32_t* __restrict__ load,
-         adr_load_stats* stats, int32_t* hist, int32_t hist_bins, F2K K, const uint32_t* __restrict__ order) {
+         adr_load_stats* stats, int32_t* hist, int32_t hist_bins, F2K K, const uint32_t* __restrict__ order,
+         const int64_t* __restrict__ nan_flag) {
     // shared-memory batch, split by use: the power test needs (mx, my, a, b)
     // + (c, tau); only splats that pass it read (sigma, r, g, b)
     // batch arrays at a 16-byte stride, one array after the other, so one
@@ -208,16 +236,19 @@ k_render(Src src, const int64_t* __restrict__ ranges, int32_t width, int32_t hei
 
     // pixels outside the image start done (T = 0 in the implied mode: they
     // are never written)
-    f2 T = kFlagDone ? K.one : pk(in0 ? 1.0f : 0.0f, in1 ? 1.0f : 0.0f), C0 = 0ull, C1 = 0ull, C2 = 0ull;
+    f2 T = pk(in0 ? 1.0f : 0.0f, in1 ? 1.0f : 0.0f), C0 = 0ull, C1 = 0ull, C2 = 0ull;
     int cnt0 = 0, cnt1 = 0;
-    bool fdone0 = !in0, fdone1 = !in1;
 #ifdef ADR_RENDER_PROFILE
     unsigned long long rp[8] = {0, 0, 0, 0, 0, 0, 0, 0};
 #endif
-#define DONE0 (kFlagDone ? fdone0 : lo_of(T) < term)
-#define DONE1 (kFlagDone ? fdone1 : hi_of(T) < term)
+#define DONE0 (lo_of(T) < term)
+#define DONE1 (hi_of(T) < term)
+    int64_t stop = end;   // first batch at whose start every pixel was done
     for (int64_t b = start; b < end; b += kBatch) {
-        if (__syncthreads_count(DONE0 && DONE1) == kRenderThreads) break;
+        if (__syncthreads_count(DONE0 && DONE1) == kRenderThreads) {
+            stop = b;
+            break;
+        }
         const int nb = (int)((end - b) < kBatch ? (end - b) : kBatch);
         for (int i = threadIdx.x; i < nb; i += kRenderThreads) {
             const Record r = src.load(b + i);
@@ -257,8 +288,6 @@ k_render(Src src, const int64_t* __restrict__ ranges, int32_t width, int32_t hei
                         bool d0f = DONE0, d1f = DONE1;
                         blend_scalar(fpx0, fpy, G, Tc, W, alpha_low, term, t0, a0, b0, d0, cnt0, d0f);
                         blend_scalar(fpx1, fpy, G, Tc, W, alpha_low, term, t1, a1, b1, d1, cnt1, d1f);
-                        fdone0 = d0f;
-                        fdone1 = d1f;
                         T = pk(t0, t1);
                         C0 = pk(a0, a1);
                         C1 = pk(b0, b1);
@@ -303,10 +332,6 @@ k_render(Src src, const int64_t* __restrict__ ranges, int32_t width, int32_t hei
                     T = mul2(T, sub2(K.one, A, K), K);
                     inc_if(cnt0, p0);
                     inc_if(cnt1, p1);
-                    if (kFlagDone) {
-                        if (p0 && lo_of(T) < term) fdone0 = true;
-                        if (p1 && hi_of(T) < term) fdone1 = true;
-                    }
                 }
                 if (__all_sync(kFull, DONE0 && DONE1)) break;
             }
@@ -323,6 +348,18 @@ k_render(Src src, const int64_t* __restrict__ ranges, int32_t width, int32_t hei
         if (lane == 0) atomicAdd(&g_render_prof[k], v);
     }
 #endif
+    uint32_t poison = 0;
+    if (!nan_flag || *nan_flag != 0) {
+        // every pixel was done at the start of batch `stop`, not at the start
+        // of the batch before: the last freeze lies in [stop - kBatch, stop)
+        int64_t pe = end;
+        if (stop < end) {
+            const int64_t rel = stop - kBatch - start > 0 ? stop - kBatch - start : 0;
+            const int64_t ce = start + (rel / kPairChunk + 1) * kPairChunk;
+            pe = ce < end ? ce : end;
+        }
+        poison = poison_bits(src, start, pe);
+    }
     const float t0 = lo_of(T), t1 = hi_of(T);
     const float o[2][3] = {{__fadd_rn(lo_of(C0), __fmul_rn(t0, bg0)), __fadd_rn(lo_of(C1), __fmul_rn(t0, bg1)),
                             __fadd_rn(lo_of(C2), __fmul_rn(t0, bg2))},
@@ -337,7 +374,7 @@ k_render(Src src, const int64_t* __restrict__ ranges, int32_t width, int32_t hei
 #pragma unroll
         for (int ch = 0; ch < 3; ++ch) {
             const float v = o[k][ch];
-            pixels[3 * pix + ch] = v < 0.f ? 0.f : (v > 1.f ? 1.f : v);
+            pixels[3 * pix + ch] = (poison >> ch) & 1u ? __int_as_float(0x7fc00000) : (v < 0.f ? 0.f : (v > 1.f ? 1.f : v));
         }
         load[pix] = cnts[k];
         if (hist) atomicAdd(hist + (cnts[k] < hist_bins ? cnts[k] : hist_bins - 1), 1);
@@ -381,6 +418,61 @@ k_render(Src src, const int64_t* __restrict__ ranges, int32_t width, int32_t hei
             atomicMin(&stats->min, mn);
             atomicMax(&stats->max, mx);
         }
+    }
+}
+
+// term_threshold > 1 or NaN (sb/render.py:100-120 taken literally): no pair
+// is ever live (T_before = 1 < term, or any comparison with NaN), so nothing
+// is composited and no count accrues.  With term > 1 every pixel freezes at
+// the span's first pair with T = 1 - eff(first pair); with a NaN term nothing
+// freezes and T = prod(1 - eff) over the whole span.  Output T * bg (C = 0),
+// plus NaN-colour poisoning over the processed chunks.  One thread per pixel.
+template <class Src>
+__global__ void __launch_bounds__(kTilePixels)
+k_render_unlit(Src src, const int64_t* __restrict__ ranges, int32_t width, int32_t height, int32_t tiles_x,
+               float bg0, float bg1, float bg2, float alpha_low, float term, float* __restrict__ pixels,
+               int32_t* __restrict__ load, adr_load_stats* stats, int32_t* hist, int32_t hist_bins,
+               const int64_t* __restrict__ nan_flag) {
+    const int tile = blockIdx.x;
+    const int ty = tile / tiles_x, tx = tile - ty * tiles_x;
+    const int px = tx * kTile + (threadIdx.x & (kTile - 1)), py = ty * kTile + (threadIdx.x >> 4);
+    const bool in = px < width && py < height;
+    const int64_t start = ranges[2 * tile], end = ranges[2 * tile + 1];
+    const bool first_only = term > 1.0f;
+    const int64_t last = first_only ? (start < end ? start + 1 : start) : end;
+    const float fpx = (float)px, fpy = (float)py;
+    float T = 1.0f;
+    for (int64_t j = start; j < last; ++j) {
+        const Record r = src.load(j);
+        const float dx = __fsub_rn(fpx, r.a.x), dy = __fsub_rn(fpy, r.a.y);
+        const float q = __fadd_rn(__fmul_rn(__fmul_rn(r.a.z, dx), dx), __fmul_rn(__fmul_rn(r.b.x, dy), dy));
+        const float power = __fsub_rn(__fmul_rn(-0.5f, q), __fmul_rn(__fmul_rn(r.a.w, dx), dy));
+        float alpha = __fmul_rn(r.b.y, exp_np(power));
+        alpha = alpha < 0.99f ? alpha : (alpha != alpha ? alpha : 0.99f);
+        T = __fmul_rn(T, __fsub_rn(1.0f, alpha >= alpha_low ? alpha : 0.0f));
+    }
+    uint32_t poison = 0;
+    if (!nan_flag || *nan_flag != 0) {
+        const int64_t ce = start + kPairChunk;
+        poison = poison_bits(src, start, first_only && ce < end ? ce : end);
+    }
+    if (in) {
+        const int64_t pix = (int64_t)py * width + px;
+        const float bg[3] = {bg0, bg1, bg2};
+#pragma unroll
+        for (int ch = 0; ch < 3; ++ch) {
+            const float v = __fadd_rn(0.0f, __fmul_rn(T, bg[ch]));
+            pixels[3 * pix + ch] = (poison >> ch) & 1u ? __int_as_float(0x7fc00000) : (v < 0.f ? 0.f : (v > 1.f ? 1.f : v));
+        }
+        load[pix] = 0;
+    }
+    const int n_in = __syncthreads_count(in);
+    if (threadIdx.x == 0 && n_in > 0) {
+        if (stats) {
+            atomicMin(&stats->min, 0);
+            atomicMax(&stats->max, 0);
+        }
+        if (hist && hist_bins > 0) atomicAdd(hist, n_in);
     }
 }
 
@@ -439,14 +531,22 @@ int32_t launch_render(const RenderArgs& a, cudaStream_t st) {
     const int64_t n_tiles = (int64_t)a.tiles_x * a.tiles_y;
     if (n_tiles <= 0) return ADR_OK;
     RecSource src{a.rec, a.idx};
+    if (!(a.term <= 1.0f)) {
+        k_render_unlit<RecSource><<<n_tiles, kTilePixels, 0, st>>>(src, a.ranges, a.width, a.height, a.tiles_x,
+                                                                   a.bg[0], a.bg[1], a.bg[2], a.alpha_low, a.term,
+                                                                   a.pixels, a.load, a.stats, a.hist, a.hist_bins,
+                                                                   a.nan_flag);
+        ADR_LAUNCH_CHECK();
+        return ADR_OK;
+    }
     if (a.order) {
         k_tile_order<<<1, 1024, 0, st>>>(a.ranges, (int32_t)n_tiles, a.order);
         ADR_LAUNCH_CHECK();
     }
-    auto kern = a.term <= 1.0f ? k_render<RecSource, false> : k_render<RecSource, true>;
-    kern<<<n_tiles, kRenderThreads, 0, st>>>(src, a.ranges, a.width, a.height, a.tiles_x, a.bg[0], a.bg[1], a.bg[2],
-                                             a.alpha_low, a.term, a.pixels, a.load, a.stats, a.hist, a.hist_bins,
-                                             f2k_host(), a.order);
+    k_render<RecSource><<<n_tiles, kRenderThreads, 0, st>>>(src, a.ranges, a.width, a.height, a.tiles_x, a.bg[0],
+                                                            a.bg[1], a.bg[2], a.alpha_low, a.term, a.pixels, a.load,
+                                                            a.stats, a.hist, a.hist_bins, f2k_host(), a.order,
+                                                            a.nan_flag);
     ADR_LAUNCH_CHECK();
     return ADR_OK;
 }
@@ -458,9 +558,15 @@ int32_t launch_render_proj(const adr_projection& p, const int64_t* gidx, const i
     const int64_t n_tiles = (int64_t)tx * ty;
     if (n_tiles <= 0) return ADR_OK;
     ProjSource src{reinterpret_cast<const float2*>(p.d_mean2d), p.d_conic, p.d_opacity, p.d_color, gidx, alpha_low};
-    auto kern = term <= 1.0f ? k_render<ProjSource, false> : k_render<ProjSource, true>;
-    kern<<<n_tiles, kRenderThreads, 0, st>>>(src, ranges, width, height, tx, bg[0], bg[1], bg[2], alpha_low, term,
-                                             pixels, load, stats, hist, bins, f2k_host(), nullptr);
+    if (!(term <= 1.0f)) {
+        k_render_unlit<ProjSource><<<n_tiles, kTilePixels, 0, st>>>(src, ranges, width, height, tx, bg[0], bg[1],
+                                                                    bg[2], alpha_low, term, pixels, load, stats,
+                                                                    hist, bins, nullptr);
+    } else {
+        k_render<ProjSource><<<n_tiles, kRenderThreads, 0, st>>>(src, ranges, width, height, tx, bg[0], bg[1], bg[2],
+                                                                 alpha_low, term, pixels, load, stats, hist, bins,
+                                                                 f2k_host(), nullptr, nullptr);
+    }
     ADR_LAUNCH_CHECK();
     return ADR_OK;
 }

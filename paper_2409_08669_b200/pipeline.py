@@ -18,6 +18,7 @@ Stage → kernels (csrc/):
 from __future__ import annotations
 
 import ctypes
+import threading
 from dataclasses import dataclass
 
 from . import _lib
@@ -77,7 +78,11 @@ class RenderStats:
 
 @dataclass(eq=False)
 class PipelineResult:
-    """sb/pipeline.py:77-82, plus the epilogue's exact load statistics."""
+    """sb/pipeline.py:77-82, plus the epilogue's exact load statistics and
+    two frame diagnostics: ``ambiguous_extents`` (culling extents whose ceil
+    could change under a last-bit change of the fp64 log — 0 proves they
+    equal numpy's, see csrc/adr_common.cuh:ceil_ambiguous) and
+    ``nan_colors`` (valid Gaussians with a NaN colour channel)."""
 
     image: Image
     load_map: LoadMap
@@ -85,6 +90,32 @@ class PipelineResult:
     projection: Projection
     pairs: TilePairList
     load_stats: LoadStats = None
+    ambiguous_extents: int = 0
+    nan_colors: int = 0
+
+
+class StaleGraphError(RuntimeError):
+    """A captured frame graph outlived the buffers it points at."""
+
+
+class FrameGraph:
+    """A CUDA graph of one frame, bound to its Rasterizer's buffer generation.
+
+    Growing the pair capacity reallocates the buffers the graph's kernels
+    point at; replaying a graph captured before that would touch freed
+    memory, so ``replay`` refuses (``StaleGraphError``).  After a replay,
+    ``Rasterizer.truncated()`` tells whether the frame needed more pairs than
+    the capacity (its outputs are then incomplete)."""
+
+    def __init__(self, graph, rast: "Rasterizer"):
+        self.graph = graph
+        self.rast = rast
+        self.generation = rast.generation
+
+    def replay(self) -> None:
+        if self.generation != self.rast.generation:
+            raise StaleGraphError("pair buffers were reallocated after capture; capture again")
+        self.graph.replay()
 
 
 def _estimate_capacity(n: int) -> int:
@@ -115,6 +146,7 @@ class Rasterizer:
         self.counters = torch.zeros(8, dtype=torch.int64, device=dev)
         self.stats = torch.zeros(3, dtype=torch.int64, device=dev)  # adr_load_stats (24 B)
         self.cap = 0
+        self.generation = 0   # bumped whenever the pair buffers are reallocated
         self.keys = self.gidx = self.scratch = None
         self._ensure_capacity(pair_capacity or _estimate_capacity(self.n))
         self.events = None
@@ -141,6 +173,7 @@ class Rasterizer:
         nbytes = _lib.lib().adr_frame_scratch_bytes(self.n, self.width, self.height, cap)
         self.scratch = torch.empty(nbytes, dtype=torch.uint8, device=dev)
         self.cap = cap
+        self.generation += 1
 
     def fit_capacity(self, pairs: int, slack: float = 1.02) -> None:
         """Size the pair buffers to `pairs` (+slack): grids of the pair-parallel
@@ -186,6 +219,11 @@ class Rasterizer:
     def pair_count(self) -> int:
         return int(self.counters[0].item())
 
+    def truncated(self) -> bool:
+        """True when the last frame needed more pairs than the capacity: its
+        pair list, ranges and image are incomplete (counters[6]; syncs)."""
+        return bool(self.counters[6].item())
+
     def render(self, scene, cam, mode=CullingMode.AABB, alpha_low=ALPHA_LOW,
                dilation=COV_DILATION, term_threshold=TERMINATION_THRESHOLD) -> PipelineResult:
         """One frame with stage timing; grows the pair buffers and re-runs when
@@ -201,10 +239,9 @@ class Rasterizer:
         while True:
             self.launch(ds, cam, mode, alpha_low, dilation, term_threshold, timed=True)
             torch.cuda.synchronize(self.device)
-            p = self.pair_count()
-            if p <= self.cap:
+            if not self.truncated():
                 break
-            self._ensure_capacity(int(p * 1.25) + 1024)
+            self._ensure_capacity(int(self.pair_count() * 1.25) + 1024)
         return self.result(mode, alpha_low)
 
     def result(self, mode, alpha_low) -> PipelineResult:
@@ -231,13 +268,15 @@ class Rasterizer:
         pairs = TilePairList(keys=keys, gaussian_indices=self.gidx[:p], tile_ranges=self.ranges)
         return PipelineResult(image=Image(self.width, self.height, self.pixels),
                               load_map=LoadMap(self.width, self.height, self.load), stats=stats,
-                              projection=self.proj, pairs=pairs, load_stats=load_stats)
+                              projection=self.proj, pairs=pairs, load_stats=load_stats,
+                              ambiguous_extents=int(ctr[5]), nan_colors=int(ctr[4]))
 
     def capture(self, scene: DeviceScene, cam, mode=CullingMode.AABB, alpha_low=ALPHA_LOW,
                 dilation=COV_DILATION, term_threshold=TERMINATION_THRESHOLD):
-        """Capture one whole frame into a CUDA graph (replay with ``g.replay()``).
+        """Capture one whole frame into a ``FrameGraph`` (replay with ``g.replay()``).
 
-        The capacity must already hold the frame's pairs (run ``render`` once)."""
+        The capacity must already hold the frame's pairs (run ``render`` once);
+        a replay whose frame outgrows it sets ``truncated()``."""
         import torch
 
         g = torch.cuda.CUDAGraph()
@@ -250,10 +289,10 @@ class Rasterizer:
         with torch.cuda.graph(g, stream=s):
             self.launch(scene, cam, mode, alpha_low, dilation, term_threshold, stream=s)
         torch.cuda.synchronize(self.device)
-        return g
+        return FrameGraph(g, self)
 
 
-_capacity_cache: dict = {}
+_workspace = threading.local()   # per host thread: {(device, N, W, H): Rasterizer}
 
 
 def run_pipeline(scene, cam, mode: CullingMode = CullingMode.AABB, alpha_low: float = ALPHA_LOW,
@@ -261,8 +300,16 @@ def run_pipeline(scene, cam, mode: CullingMode = CullingMode.AABB, alpha_low: fl
                  term_threshold: float = TERMINATION_THRESHOLD) -> PipelineResult:
     """All six stages for one scene/camera/mode (sb/pipeline.py:85-124).
 
-    Returns fresh CUDA tensors owned by the caller.  ``threads`` is accepted
-    for signature compatibility and never changes any output."""
+    ``scene``: a DeviceScene (CUDA, or CPU — e.g. pinned — which is uploaded),
+    a SceneArrays / reference Scene (uploaded as fp32 when every value is
+    exactly representable, else fp64).  The frame's workspace (pair buffers,
+    scratch) is kept per (device, N, W, H) and host thread and reused; the
+    returned arrays are fresh CUDA tensors owned by the caller, with the
+    reference's dtypes (gaussian_indices int64, keys uint64 bit patterns).
+    ``threads`` is accepted for signature compatibility and never changes
+    any output."""
+    import torch
+
     mode = CullingMode(mode)
     grid = TileGrid(width=cam.width, height=cam.height)
     if not 0.0 < alpha_low < 1.0:
@@ -270,9 +317,21 @@ def run_pipeline(scene, cam, mode: CullingMode = CullingMode.AABB, alpha_low: fl
     if dilation < 0:
         raise ValueError("dilation must be non-negative")
     ds = as_device_scene(scene)
+    cache = getattr(_workspace, "rast", None)
+    if cache is None:
+        cache = _workspace.rast = {}
     key = (str(ds.device), len(ds), grid.width, grid.height)
-    r = Rasterizer(grid.width, grid.height, len(ds), device=ds.device,
-                   pair_capacity=_capacity_cache.get(key, 0))
+    r = cache.get(key)
+    if r is None:
+        r = cache[key] = Rasterizer(grid.width, grid.height, len(ds), device=ds.device)
     res = r.render(ds, cam, mode, alpha_low, dilation, term_threshold)
-    _capacity_cache[key] = max(r.cap, _capacity_cache.get(key, 0))
-    return res
+    # hand the caller its own copies; the workspace stays with the cache
+    p = res.stats.pair_count
+    pairs = TilePairList(keys=r.keys[:p].clone() if r.export_pairs else None,
+                         gaussian_indices=r.gidx[:p].to(torch.int64),
+                         tile_ranges=r.ranges.clone())
+    return PipelineResult(image=Image(r.width, r.height, r.pixels.clone()),
+                          load_map=LoadMap(r.width, r.height, r.load.clone()),
+                          stats=res.stats, projection=r.proj.clone(), pairs=pairs,
+                          load_stats=res.load_stats, ambiguous_extents=res.ambiguous_extents,
+                          nan_colors=res.nan_colors)

@@ -70,6 +70,10 @@ class Projection:
     def to_numpy(self) -> dict:
         return {name: getattr(self, name).cpu().numpy() for name in _ARRAY_FIELDS}
 
+    def clone(self) -> "Projection":
+        return Projection(mode=self.mode, alpha_low=self.alpha_low,
+                          **{name: getattr(self, name).clone() for name in _ARRAY_FIELDS})
+
     @classmethod
     def empty(cls, n: int, mode, alpha_low, device) -> "Projection":
         import torch
@@ -98,10 +102,13 @@ class Projection:
 
 
 def as_device_scene(scene, device=None) -> DeviceScene:
+    """The scene on a CUDA device: a CUDA DeviceScene as is, a host one (e.g.
+    pinned) uploaded, anything else converted (DeviceScene.from_scene)."""
     import torch
 
     if device is None:
-        device = scene.device if isinstance(scene, DeviceScene) else torch.device("cuda")
+        on_cuda = isinstance(scene, DeviceScene) and scene.device.type == "cuda"
+        device = scene.device if on_cuda else torch.device("cuda")
     return DeviceScene.from_scene(scene, device=device)
 
 

@@ -206,6 +206,19 @@ def generate_synthetic(seed: int, count: int, spec: SyntheticSpec | None = None)
     return Scene(gaussians=gs, sh_degree=0)
 
 
+def _exact_in_f32(a: np.ndarray) -> bool:
+    if a.dtype == np.float32:
+        return True
+    if a.dtype != np.float64:
+        return False
+    with np.errstate(over="ignore", invalid="ignore"):
+        return bool(np.array_equal(a.astype(np.float32).astype(np.float64), a, equal_nan=True))
+
+
+def _aligned(t, align: int = 16):
+    return t if t.data_ptr() % align == 0 else t.clone()
+
+
 class DeviceScene:
     """SoA scene resident on the GPU (what ``adr_scene`` points at).
 
@@ -227,8 +240,10 @@ class DeviceScene:
         n = ts[3].numel()
         k = (sh_degree + 1) ** 2
         shapes = [(n, 3), (n, 3), (n, 4), (n,), (n, k, 3)]
+        # contiguous and 16-byte aligned (the preprocess stages the SH slab
+        # with 16-byte vector loads): an offset view is copied
         self.centers, self.scales, self.rotations, self.opacities, self.sh = (
-            t.reshape(s).contiguous() for t, s in zip(ts, shapes))
+            _aligned(t.reshape(s).contiguous()) for t, s in zip(ts, shapes))
         self.sh_degree = int(sh_degree)
 
     def __len__(self) -> int:
@@ -240,10 +255,17 @@ class DeviceScene:
 
     @classmethod
     def from_arrays(cls, arrays, sh_degree: int, device="cuda", dtype=None) -> "DeviceScene":
+        """Upload host arrays.  ``dtype=None`` picks float32 when every value
+        is exactly representable in it (the fp32 -> fp64 promotion inside the
+        kernel then reproduces the fp64 inputs bit for bit, at half the
+        bytes), else float64."""
         import torch
 
-        dtype = dtype or torch.float64
-        return cls(*(torch.as_tensor(np.ascontiguousarray(a), dtype=dtype).to(device)
+        arrays = [np.asarray(a) for a in arrays]
+        if dtype is None:
+            dtype = torch.float32 if all(_exact_in_f32(a) for a in arrays) else torch.float64
+        np_dt = np.float32 if dtype == torch.float32 else np.float64
+        return cls(*(torch.from_numpy(np.ascontiguousarray(a, dtype=np_dt)).to(device)
                      for a in arrays), sh_degree=sh_degree)
 
     @classmethod

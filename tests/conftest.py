@@ -16,6 +16,9 @@ if str(ROOT) not in sys.path:
     sys.path.insert(0, str(ROOT))
 
 GOLDEN_CASES = ("g_sh0_aabb", "g_sh3_baseline", "g_sh3_circle", "g_sh2_near_aabb", "g_sh1_small_aabb")
+# edge semantics goldens (make_semantics_golden.py): term > 1, NaN term, NaN
+# SH colours (chunked poisoning), extents beyond int32
+SEMANTIC_CASES = ("g_term_gt1", "g_term_nan", "g_nan_sh", "g_huge_extent")
 PROJ_FIELDS = ("valid", "mean2d", "cov2d", "conic", "depth", "color", "opacity", "lambda_max",
                "ext_x", "ext_y")
 
@@ -68,6 +71,20 @@ def bits_equal(a, b) -> bool:
     b = np.ascontiguousarray(b)
     return a.shape == b.shape and a.dtype.itemsize == b.dtype.itemsize and \
         np.array_equal(a.view(np.uint8), b.view(np.uint8))
+
+
+def nan_bits_equal(a, b) -> bool:
+    """Bit-exact, except that NaNs only need to be NaN in both (payloads of
+    NaNs from NaN inputs are platform-specific)."""
+    a = np.ascontiguousarray(a)
+    b = np.ascontiguousarray(b)
+    if a.shape != b.shape or a.dtype.itemsize != b.dtype.itemsize:
+        return False
+    if a.dtype.kind != "f":
+        return np.array_equal(a.view(np.uint8), b.view(np.uint8))
+    na, nb = np.isnan(a), np.isnan(b)
+    u = np.uint32 if a.dtype.itemsize == 4 else np.uint64
+    return bool(np.array_equal(na, nb) and np.array_equal(a.view(u)[~na], b.view(u)[~nb]))
 
 
 def make_camera(width=64, height=64, distance=5.0, fov=60.0, background=(0.0, 0.0, 0.0)):
