@@ -407,7 +407,9 @@ __global__ void __launch_bounds__(256) k_ranges_search(TileIds<TileT> tiles, con
 
 }  // namespace
 
-size_t frame_binning_scratch(int64_t n, int64_t cap, int64_t n_tiles) {
+size_t frame_binning_scratch(int64_t n, int64_t cap, int32_t tiles_x, int32_t tiles_y) {
+    const int64_t n_tiles = (int64_t)tiles_x * tiles_y;
+    if (supertile_path(n_tiles, tiles_x, tiles_y)) return supertile_scratch(n, cap, tiles_x, tiles_y);
     const int64_t nc = ceil_div(n > 0 ? n : 1, 256);
     const bool wide = n_tiles > 65536;
     const size_t tile_sz = wide ? 4 : 2;
@@ -488,6 +490,7 @@ int32_t frame_binning(const FrameBinning& fb, cudaStream_t st) {
     if (fb.cap >= (int64_t(1) << 31)) return fail(ADR_ERR_CAPACITY, "pair capacity must be < 2^31");
     if (fb.tiles_x >= 65536 || fb.tiles_y >= 65536) return fail(ADR_ERR_CAPACITY, "tile grid side >= 65536");
     if (!fb.gidx) return fail(ADR_ERR_VALUE, "render_frame needs the sorted index buffer");
+    if (supertile_path(fb.n_tiles, fb.tiles_x, fb.tiles_y)) return frame_binning_supertile(fb, st);
     return fb.n_tiles > 65536 ? frame_binning_t<uint32_t>(fb, st) : frame_binning_t<uint16_t>(fb, st);
 }
 

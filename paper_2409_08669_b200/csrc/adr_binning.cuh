@@ -41,7 +41,13 @@ struct FrameBinning {
                 ev_after_ranges = nullptr;
 };
 
-size_t frame_binning_scratch(int64_t n, int64_t cap, int64_t n_tiles);
+size_t frame_binning_scratch(int64_t n, int64_t cap, int32_t tiles_x, int32_t tiles_y);
 int32_t frame_binning(const FrameBinning& fb, cudaStream_t st);
+
+// Supertile counting placement (adr_supertile.cu), used when the grid has at
+// most 1024 supertiles of 8x8 tiles (<= 65536 tiles).
+bool supertile_path(int64_t n_tiles, int32_t tiles_x, int32_t tiles_y);
+size_t supertile_scratch(int64_t n, int64_t cap, int32_t tiles_x, int32_t tiles_y);
+int32_t frame_binning_supertile(const FrameBinning& fb, cudaStream_t st);
 
 }  // namespace adr

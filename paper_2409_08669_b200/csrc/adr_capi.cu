@@ -38,7 +38,8 @@ struct FrameLayout {
     size_t binning_bytes;
 };
 
-size_t frame_bytes(int64_t n, int64_t n_tiles, int64_t cap, FrameLayout* out, void* base, size_t cap_bytes) {
+size_t frame_bytes(int64_t n, int32_t tx, int32_t ty, int64_t cap, FrameLayout* out, void* base, size_t cap_bytes) {
+    const int64_t n_tiles = (int64_t)tx * ty;
     Carver c(base, cap_bytes);
     FrameLayout l;
     l.dkey = c.take<uint32_t>(n);
@@ -46,7 +47,7 @@ size_t frame_bytes(int64_t n, int64_t n_tiles, int64_t cap, FrameLayout* out, vo
     l.rec = c.take<Record>(n);
     l.gpack = c.take<uint2>(n);
     l.tile_order = c.take<uint32_t>(n_tiles);
-    l.binning_bytes = frame_binning_scratch(n, cap, n_tiles);
+    l.binning_bytes = frame_binning_scratch(n, cap, tx, ty);
     l.binning = c.take<char>((int64_t)l.binning_bytes);
     if (out) *out = l;
     return c.used;
@@ -126,8 +127,7 @@ int32_t adr_render(const adr_projection* proj, int64_t n, const int64_t* d_gidx,
 }
 
 size_t adr_frame_scratch_bytes(int64_t n, int32_t width, int32_t height, int64_t pair_capacity) {
-    const int64_t n_tiles = (int64_t)tiles_of(width) * tiles_of(height);
-    return frame_bytes(n, n_tiles, pair_capacity, nullptr, nullptr, 0) + 1024;
+    return frame_bytes(n, tiles_of(width), tiles_of(height), pair_capacity, nullptr, nullptr, 0) + 1024;
 }
 
 int32_t adr_render_frame(const adr_scene* scene, const adr_camera* cam, int32_t mode, double alpha_low,
@@ -140,7 +140,7 @@ int32_t adr_render_frame(const adr_scene* scene, const adr_camera* cam, int32_t 
     if (n_tiles >= (int64_t(1) << 32)) return fail(ADR_ERR_CAPACITY, "tile count does not fit the 32-bit key field");
     const int64_t n = scene->n;
     FrameLayout L;
-    const size_t need = frame_bytes(n, n_tiles, buf->pair_capacity, &L, buf->d_scratch, buf->scratch_bytes);
+    const size_t need = frame_bytes(n, tx, ty, buf->pair_capacity, &L, buf->d_scratch, buf->scratch_bytes);
     if (need > buf->scratch_bytes) return fail(ADR_ERR_VALUE, "render_frame: scratch too small");
     cudaEvent_t ev[7] = {};
     if (buf->events)

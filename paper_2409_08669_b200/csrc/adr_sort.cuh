@@ -123,6 +123,7 @@ scan_u32_exclusive(uint32_t* __restrict__ data, int64_t n, uint64_t* status, uns
 // identity (value = input index).  Last-pass extras (MODE):
 //   1: exp_keys[g] = key << 32 | float bits of exp_depth[value]  (reference keys)
 //   2: gdst[g] = gsrc[value] (8-byte gather) and vals_out[g] = value; no key output
+//   3: rinfo[g] = {value, key, gsrc[value]} (16-byte rank record); no key/value output
 struct SortExtra {
     int mode = 0;
     const float* exp_depth = nullptr;
@@ -130,6 +131,7 @@ struct SortExtra {
     bool skip_keys_out = false;   // MODE 1: the exported keys carry the tile ids, no separate copy
     const uint2* gsrc = nullptr;
     uint2* gdst = nullptr;
+    uint4* rinfo = nullptr;
 };
 
 template <typename K, typename V, int RB, int MODE>
@@ -215,7 +217,10 @@ radix_downsweep(const K* __restrict__ keys_in, const V* __restrict__ vals_in, K*
         const K key = skeys[i];
         const V val = svals[i];
         const int64_t g = goff[digit_of(key, bit, R - 1)] + i;
-        if (MODE == 2) {
+        if (MODE == 3) {
+            const uint2 r = __ldg(ex.gsrc + val);
+            ex.rinfo[g] = make_uint4((uint32_t)val, (uint32_t)key, r.x, r.y);
+        } else if (MODE == 2) {
             vals_out[g] = val;
             ex.gdst[g] = __ldg(ex.gsrc + val);
         } else {
@@ -294,6 +299,11 @@ int32_t radix_sort(const K* keys_in, const V* vals_in, K* keys_out, V* vals_out,
             ADR_CUDA_TRY(cudaFuncSetAttribute(radix_downsweep<K, V, RB, 1>,                                   \
                                               cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dsm));        \
             radix_downsweep<K, V, RB, 1><<<nb, kSortBlock, dsm, st>>>(src_k, src_v, dst_k, dst_v, d_n, n_max,  \
+                                                                      bit, hist, extra);                      \
+        } else if (mode == 3) {                                                                               \
+            ADR_CUDA_TRY(cudaFuncSetAttribute(radix_downsweep<K, V, RB, 3>,                                   \
+                                              cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dsm));        \
+            radix_downsweep<K, V, RB, 3><<<nb, kSortBlock, dsm, st>>>(src_k, src_v, dst_k, dst_v, d_n, n_max,  \
                                                                       bit, hist, extra);                      \
         } else if (mode == 2) {                                                                               \
             ADR_CUDA_TRY(cudaFuncSetAttribute(radix_downsweep<K, V, RB, 2>,                                   \
