@@ -45,7 +45,8 @@ namespace adr {
 namespace {
 
 constexpr int kStSide = 8;            // supertile side in tiles
-constexpr int kL1Ranks = 256;         // ranks per L1 warp chunk (8 warp chunks per scatter block)
+constexpr int kL1Ranks = 256;         // ranks per L1 warp chunk
+constexpr int kL1Block = 8 * kL1Ranks; // ranks per L1 block (h1b column entry, scatter block)
 constexpr int kL1Cap = 4096;          // items staged per L1 scatter window
 constexpr int kChunk = 256;           // items per L2 chunk (= one 256-thread block)
 constexpr int kStageCap = 4096;       // pairs staged per placement window
@@ -127,48 +128,46 @@ __device__ __forceinline__ int stream_owner(bool has, uint32_t o, uint32_t base,
 
 // ---------------------------------------------------------------- L1
 
-// Items per (256-rank warp chunk, supertile) into H1[s * n1p + w1] (column
-// per supertile); the true pair count P (sum of rectangle areas) into *d_p.
-// The warp's 8 rectangles per lane are loaded up front.
+// Items per (2048-rank block, supertile) into H1[s * n1p + b] (one shared
+// histogram per block; each thread's 8 rectangles are loaded up front), and
+// the true pair count P (sum of rectangle areas) into *d_p.
 __global__ void __launch_bounds__(256) k_st_count1(const uint4* __restrict__ rinfo, const int64_t* __restrict__ d_m,
                                                    StGeom g, uint32_t* __restrict__ H1,
                                                    unsigned long long* __restrict__ d_p) {
-    extern __shared__ uint32_t st_smem[];
-    constexpr int kR = kL1Ranks / 32;
-    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    uint32_t* hist = st_smem + warp * g.S;
+    extern __shared__ uint32_t hist[];   // [S]
+    constexpr int kR = kL1Block / 256;
+    const int lane = threadIdx.x & 31;
     const int64_t m = *d_m;
-    const int64_t w1 = (int64_t)blockIdx.x * 8 + warp;
-    const int64_t r0 = w1 * kL1Ranks;
+    const int64_t b = blockIdx.x;
+    const int64_t r0 = b * kL1Block;
     if (r0 >= m) return;
-    const int64_t r1 = r0 + kL1Ranks < m ? r0 + kL1Ranks : m;
     uint2 rc[kR];
 #pragma unroll
     for (int k = 0; k < kR; ++k) {
-        const int64_t r = r0 + k * 32 + lane;
-        rc[k] = r < r1 ? __ldg(reinterpret_cast<const uint2*>(rinfo + r) + 1) : make_uint2(0u, 0u);
+        const int64_t r = r0 + k * 256 + threadIdx.x;
+        rc[k] = r < m ? __ldg(reinterpret_cast<const uint2*>(rinfo + r) + 1) : make_uint2(0u, 0u);
     }
-    for (int s = lane; s < g.S; s += 32) hist[s] = 0;
-    __syncwarp();
+    for (int s = threadIdx.x; s < g.S; s += 256) hist[s] = 0;
+    __syncthreads();
     uint64_t area = 0;
 #pragma unroll
     for (int k = 0; k < kR; ++k) {
         const uint32_t x0 = rc[k].x & 0xffffu, x1 = rc[k].x >> 16, y0 = rc[k].y & 0xffffu, y1 = rc[k].y >> 16;
-        if (x1 > x0) {   // ranks < M have a non-empty rectangle; padding lanes are (0, 0)
+        if (x1 > x0) {   // ranks < M have a non-empty rectangle; padding threads are (0, 0)
             area += (uint64_t)(x1 - x0) * (y1 - y0);
-            const uint32_t sx0 = x0 >> 3, sx1 = (x1 - 1) >> 3, sy0 = y0 >> 3, sy1 = (y1 - 1) >> 3;
-            for (uint32_t sy = sy0; sy <= sy1; ++sy)
-                for (uint32_t sx = sx0; sx <= sx1; ++sx) atomicAdd(&hist[sy * g.sxn + sx], 1u);
+            for (uint32_t sy = y0 >> 3; sy <= (y1 - 1) >> 3; ++sy)
+                for (uint32_t sx = x0 >> 3; sx <= (x1 - 1) >> 3; ++sx) atomicAdd(&hist[sy * g.sxn + sx], 1u);
         }
     }
-    __syncwarp();
-    for (int s = lane; s < g.S; s += 32) H1[s * g.n1p + w1] = hist[s];
+    __syncthreads();
+    for (int s = threadIdx.x; s < g.S; s += 256) H1[s * g.n1p + b] = hist[s];
     area = warp_sum(area);
-    if (lane == 0) atomicAdd(d_p, (unsigned long long)area);
+    if (lane == 0 && area) atomicAdd(d_p, (unsigned long long)area);
 }
 
-// Exclusive scan of every supertile column of H1 over the warp chunks (block
-// per supertile; per batch each thread holds 8 consecutive rows, loaded as two
+// Exclusive scan of every supertile column of H1 (items per 2048-rank block,
+// counted by the depth sort's last pass) over the blocks (block per
+// supertile; per batch each thread holds 8 consecutive rows, loaded as two
 // 16-byte vectors), the bucket totals, and (last block) the padded bucket
 // starts, the bucket ends and the chunk -> supertile / unit -> chunk maps.
 __global__ void __launch_bounds__(1024) k_st_scan1(uint32_t* __restrict__ H1, const int64_t* __restrict__ d_m,
@@ -183,7 +182,7 @@ __global__ void __launch_bounds__(1024) k_st_scan1(uint32_t* __restrict__ H1, co
         stats->min = INT_MAX;
         stats->max = INT_MIN;
     }
-    const int64_t n1 = (*d_m + kL1Ranks - 1) / kL1Ranks;
+    const int64_t n1 = (*d_m + kL1Block - 1) / kL1Block;
     uint32_t* col = H1 + blockIdx.x * g.n1p;
     uint32_t carry = 0;
     for (int64_t b0 = 0; b0 < n1; b0 += 1024 * K) {
@@ -223,9 +222,9 @@ __global__ void __launch_bounds__(1024) k_st_scan1(uint32_t* __restrict__ H1, co
     __syncthreads();
     if (!last) return;
     __threadfence();
-    // padded bucket starts (S <= 1024: one supertile per thread), bucket ends,
-    // units per supertile, then the chunk -> supertile and unit -> chunk maps
-    __shared__ uint32_t sp_s[1025], ub_s[1025];
+    // padded bucket starts (S <= 1024: one supertile per thread), bucket ends
+    // and the first unit of every supertile; the chunk -> supertile and
+    // unit -> chunk maps are filled by k_st_scatter1's blocks
     const int t = threadIdx.x;
     const int64_t n2cap = items_cap / kChunk;
     const uint32_t tt = t < g.S ? __ldcg(c.total + t) : 0u;
@@ -242,8 +241,6 @@ __global__ void __launch_bounds__(1024) k_st_scan1(uint32_t* __restrict__ H1, co
         c.pstart[t] = pre;
         c.iend[t] = pre + tt;
         c.ubase[t] = upre;
-        sp_s[t] = (uint32_t)ch0;
-        ub_s[t] = upre;
     }
     if (t == 0) {
         c.pstart[g.S] = all;
@@ -251,35 +248,18 @@ __global__ void __launch_bounds__(1024) k_st_scan1(uint32_t* __restrict__ H1, co
         if ((int64_t)all > items_cap) counters[6] = 1;   // cannot happen unless P > capacity
         c.ticket[0] = 0;
     }
-    __syncthreads();
-    const int64_t n2 = (int64_t)all / kChunk < n2cap ? (int64_t)all / kChunk : n2cap;
-    for (int64_t ch = t; ch < n2; ch += 1024) {
-        int lo = 0, hi = g.S - 1;   // last supertile whose first chunk <= ch
-        while (lo < hi) {
-            const int mid = (lo + hi + 1) >> 1;
-            if ((int64_t)sp_s[mid] <= ch) lo = mid; else hi = mid - 1;
-        }
-        c.cmap[ch] = (uint16_t)lo;
-    }
-    for (uint32_t u = t; u < all_units; u += 1024) {
-        int lo = 0, hi = g.S - 1;   // last supertile whose first unit <= u
-        while (lo < hi) {
-            const int mid = (lo + hi + 1) >> 1;
-            if (ub_s[mid] <= u) lo = mid; else hi = mid - 1;
-        }
-        c.umap[u] = sp_s[lo] + (u - ub_s[lo]) * kUnit;
-    }
 }
 
 // Place the items, stably in rank order within each supertile bucket.  Block
-// = 8 warp chunks (2048 ranks).  Per round of 32 ranks a warp's items form a
+// = 2048 ranks, warp = 256 ranks (held in registers: a per-warp supertile
+// histogram first, then the placement).  Per round of 32 ranks a warp's items form a
 // stream in (rank, supertile) order; lanes take consecutive stream positions
 // (balanced however many supertiles a rank touches), peers with the same
 // supertile come from match.any and the lowest peer bumps the warp's running
 // offset.  Items are staged in shared memory in bucket order (the block's
 // items of one supertile are contiguous in the output) and flushed as
 // coalesced runs.
-__global__ void __launch_bounds__(256) k_st_scatter1(const uint4* __restrict__ rinfo, const int64_t* __restrict__ d_m,
+__global__ void __launch_bounds__(256, 4) k_st_scatter1(const uint4* __restrict__ rinfo, const int64_t* __restrict__ d_m,
                                                      StGeom g, const uint32_t* __restrict__ H1, StCtl c,
                                                      StItems items, int64_t items_cap) {
     extern __shared__ __align__(16) unsigned char sc_raw[];
@@ -294,10 +274,29 @@ __global__ void __launch_bounds__(256) k_st_scatter1(const uint4* __restrict__ r
     constexpr int kR = kL1Ranks / 32;
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const int64_t m = *d_m;
-    const int64_t n1 = (m + kL1Ranks - 1) / kL1Ranks;
-    const int64_t wb0 = (int64_t)blockIdx.x * 8;
-    if (wb0 * kL1Ranks >= m) return;
-    // per supertile: block total, warp bases, global start of the block's run
+    const int64_t b = blockIdx.x;
+    const int64_t r0 = b * kL1Block + warp * kL1Ranks;
+    const int64_t r1 = r0 + kL1Ranks < m ? r0 + kL1Ranks : m;
+    // this warp's ranks, and its items per supertile (shared-memory histogram)
+    uint4 vb[kR];
+#pragma unroll
+    for (int k = 0; k < kR; ++k) {
+        const int64_t r = r0 + k * 32 + lane;
+        vb[k] = r < r1 ? rinfo[r] : make_uint4(0u, 0u, 0u, 0u);
+    }
+    uint32_t* wh = wbase + warp * g.S;
+    for (int s = lane; s < g.S; s += 32) wh[s] = 0;
+    __syncwarp();
+#pragma unroll
+    for (int k = 0; k < kR; ++k) {
+        const uint32_t x0 = vb[k].z & 0xffffu, x1 = vb[k].z >> 16, y0 = vb[k].w & 0xffffu, y1 = vb[k].w >> 16;
+        if (x1 > x0)
+            for (uint32_t sy = y0 >> 3; sy <= (y1 - 1) >> 3; ++sy)
+                for (uint32_t sx = x0 >> 3; sx <= (x1 - 1) >> 3; ++sx) atomicAdd(&wh[sy * g.sxn + sx], 1u);
+    }
+    __syncthreads();
+    // per supertile: per-warp exclusive prefixes (in place), block total,
+    // block-local bucket start and the global start of the block's run
     uint32_t mysum = 0;
     constexpr int kPer = 4;   // supertiles per thread (S <= 1024)
     uint32_t bt[kPer];
@@ -306,12 +305,15 @@ __global__ void __launch_bounds__(256) k_st_scatter1(const uint4* __restrict__ r
         const int s = threadIdx.x * kPer + k;
         bt[k] = 0;
         if (s < g.S) {
-            const uint32_t* colp = H1 + s * g.n1p + wb0;
-            const uint32_t v0 = colp[0];
+            uint32_t run = 0;
 #pragma unroll
-            for (int w = 0; w < 8; ++w) wbase[w * g.S + s] = wb0 + w < n1 ? colp[w] - v0 : 0u;
-            bt[k] = (wb0 + 8 < n1 ? colp[8] : __ldg(c.total + s)) - v0;
-            g0[s] = __ldg(c.pstart + s) + v0;
+            for (int w = 0; w < 8; ++w) {
+                const uint32_t v = wbase[w * g.S + s];
+                wbase[w * g.S + s] = run;
+                run += v;
+            }
+            bt[k] = run;
+            g0[s] = __ldg(c.pstart + s) + H1[s * g.n1p + b];
         }
         mysum += bt[k];
     }
@@ -323,22 +325,38 @@ __global__ void __launch_bounds__(256) k_st_scatter1(const uint4* __restrict__ r
         if (s < g.S) lst[s] = run;
         run += bt[k];
     }
+    // this block's share of the chunk -> supertile and unit -> chunk maps
+    {
+        const int64_t n2cap = items_cap / kChunk;
+        int64_t n2 = __ldg(c.pstart + g.S) / kChunk;
+        n2 = n2 < n2cap ? n2 : n2cap;
+        const int64_t per = (n2 + gridDim.x - 1) / gridDim.x;
+        for (int64_t ch = b * per + threadIdx.x; ch < (b + 1) * per && ch < n2; ch += 256) {
+            int lo = 0, hi = g.S - 1;   // last supertile whose first chunk <= ch
+            while (lo < hi) {
+                const int mid = (lo + hi + 1) >> 1;
+                if ((int64_t)(__ldg(c.pstart + mid) / kChunk) <= ch) lo = mid; else hi = mid - 1;
+            }
+            c.cmap[ch] = (uint16_t)lo;
+        }
+        const uint32_t nu = __ldg(c.ubase + g.S);
+        const uint32_t uper = (nu + gridDim.x - 1) / gridDim.x;
+        for (uint32_t u = (uint32_t)b * uper + threadIdx.x; u < ((uint32_t)b + 1) * uper && u < nu; u += 256) {
+            int lo = 0, hi = g.S - 1;   // last supertile whose first unit <= u
+            while (lo < hi) {
+                const int mid = (lo + hi + 1) >> 1;
+                if (__ldg(c.ubase + mid) <= u) lo = mid; else hi = mid - 1;
+            }
+            c.umap[u] = __ldg(c.pstart + lo) / kChunk + (u - __ldg(c.ubase + lo)) * kUnit;
+        }
+    }
     __syncthreads();
-    const int64_t w1 = wb0 + warp;
-    const int64_t r0 = w1 * kL1Ranks;
-    const int64_t r1 = r0 + kL1Ranks < m ? r0 + kL1Ranks : m;
     const uint32_t lt = (1u << lane) - 1u;
     uint32_t* off = woff + warp * g.S;
     for (uint32_t win = 0; win < btotal; win += kL1Cap) {
         for (int s = lane; s < g.S; s += 32) off[s] = lst[s] + wbase[warp * g.S + s];
         __syncwarp();
         if (r0 < r1) {
-            uint4 vb[kR];
-#pragma unroll
-            for (int k = 0; k < kR; ++k) {
-                const int64_t r = r0 + k * 32 + lane;
-                vb[k] = r < r1 ? rinfo[r] : make_uint4(0u, 0u, 0u, 0u);
-            }
 #pragma unroll
             for (int k = 0; k < kR; ++k) {
                 const uint4 v = vb[k];
@@ -501,19 +519,31 @@ __global__ void __launch_bounds__(1024) k_st_scan2(uint32_t* __restrict__ U, StG
     __syncthreads();
     if (!last) return;
     __threadfence();
-    // tile starts in tile order, ranges, P (counted) and P clamped to capacity
+    // tile starts in tile order, ranges, P (counted) and P clamped to capacity;
+    // each thread scans a run of up to 8 consecutive tiles per batch
     uint64_t acc = 0;
-    for (int64_t t0 = 0; t0 < n_tiles; t0 += 1024) {
-        const int64_t t = t0 + threadIdx.x;
-        const uint64_t v = t < n_tiles ? __ldcg(c.ttot + t) : 0ull;
+    for (int64_t t0 = 0; t0 < n_tiles; t0 += 1024 * 8) {
+        const int64_t a = t0 + (int64_t)threadIdx.x * 8;
+        uint32_t v[8];
+        uint64_t sum = 0;
+#pragma unroll
+        for (int k = 0; k < 8; ++k) {
+            v[k] = a + k < n_tiles ? __ldcg(c.ttot + a + k) : 0u;
+            sum += v[k];
+        }
         uint64_t blk;
-        const uint64_t pre = acc + block_exclusive_sum<uint64_t, 1024>(v, sred, &blk);
-        if (t < n_tiles) {
-            c.tstart[t] = pre < 0xffffffffull ? (uint32_t)pre : 0xffffffffu;
-            const int64_t lo = (int64_t)pre < cap ? (int64_t)pre : cap;
-            const int64_t hi = (int64_t)(pre + v) < cap ? (int64_t)(pre + v) : cap;
-            ranges[2 * t] = lo;
-            ranges[2 * t + 1] = hi;
+        uint64_t pre = acc + block_exclusive_sum<uint64_t, 1024>(sum, sred, &blk);
+#pragma unroll
+        for (int k = 0; k < 8; ++k) {
+            const int64_t t = a + k;
+            if (t < n_tiles) {
+                c.tstart[t] = pre < 0xffffffffull ? (uint32_t)pre : 0xffffffffu;
+                const int64_t lo = (int64_t)pre < cap ? (int64_t)pre : cap;
+                const int64_t hi = (int64_t)(pre + v[k]) < cap ? (int64_t)(pre + v[k]) : cap;
+                ranges[2 * t] = lo;
+                ranges[2 * t + 1] = hi;
+            }
+            pre += v[k];
         }
         acc += blk;
     }
@@ -672,7 +702,7 @@ static int64_t st_items_cap(int64_t cap, int64_t S) { return cap + (int64_t)kChu
 
 size_t supertile_scratch(int64_t n, int64_t cap, int32_t tx, int32_t ty) {
     const int64_t S = supertile_count(tx, ty), T = (int64_t)tx * ty;
-    const int64_t n1p = align_up(ceil_div(n > 0 ? n : 1, kL1Ranks) + 8, 8);
+    const int64_t n1p = align_up(ceil_div(n > 0 ? n : 1, kL1Block) + 8, 8);
     const int64_t icap = st_items_cap(cap, S);
     size_t s = 0;
     s += align_up(16 * (size_t)n);               // rinfo
@@ -704,9 +734,8 @@ int32_t frame_binning_supertile(const FrameBinning& fb, cudaStream_t st) {
     g.syn = (int32_t)ceil_div(g.ty, kStSide);
     g.S = g.sxn * g.syn;
     g.rsxn = 1.0f / (float)g.sxn;
-    g.n1p = (int64_t)align_up(ceil_div(n, kL1Ranks) + 8, 8);
+    g.n1p = (int64_t)align_up(ceil_div(n, kL1Block) + 8, 8);
     const int64_t T = fb.n_tiles;
-    const int64_t n1 = ceil_div(n, kL1Ranks);
     const int64_t icap = st_items_cap(cap, g.S);
     const int64_t n2max = icap / kChunk;
     Carver cv(fb.scratch, fb.scratch_bytes);
@@ -743,14 +772,14 @@ int32_t frame_binning_supertile(const FrameBinning& fb, cudaStream_t st) {
                                                 radix_scratch_bytes<uint32_t, uint32_t>(n), st, dx);
     if (rc) return rc;
     // L1: ranks -> supertile items
-    const unsigned nb1 = (unsigned)ceil_div(n1, 8);
-    k_st_count1<<<nb1, 256, 8 * g.S * sizeof(uint32_t), st>>>(rinfo, ctr + 2, g, H1,
-                                                             reinterpret_cast<unsigned long long*>(ctr));
+    const unsigned nb1 = (unsigned)ceil_div(n, kL1Block);
+    k_st_count1<<<nb1, 256, g.S * sizeof(uint32_t), st>>>(rinfo, ctr + 2, g, H1,
+                                                         reinterpret_cast<unsigned long long*>(ctr));
     ADR_LAUNCH_CHECK();
     k_st_scan1<<<(unsigned)g.S, 1024, 0, st>>>(H1, ctr + 2, g, c, icap, ctr, fb.stats);
     ADR_LAUNCH_CHECK();
     if (fb.ev_after_scan) ADR_CUDA_TRY(cudaEventRecord(fb.ev_after_scan, st));
-    const size_t sm_sc = 12 * (size_t)kL1Cap + (18 * (size_t)g.S + 2) * sizeof(uint32_t);
+    const size_t sm_sc = 12 * (size_t)kL1Cap + (18 * (size_t)g.S + 2) * sizeof(uint32_t);  // see k_st_scatter1
     ADR_CUDA_TRY(cudaFuncSetAttribute(k_st_scatter1, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm_sc));
     k_st_scatter1<<<nb1, 256, sm_sc, st>>>(rinfo, ctr + 2, g, H1, c, items, icap);
     ADR_LAUNCH_CHECK();
