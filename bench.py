@@ -1,19 +1,24 @@
 #!/usr/bin/env python
 """Benchmark: rendered frames/s and Gaussian-tile pairs/frame (BASELINE.json).
 
-    python bench.py [--gpus N --steps K --warmup W] [--config garden] [--impl ours|reference]
+    python bench.py [--gpus N --steps K --warmup W] [--config garden] [--views V] [--impl ours|reference]
 
-One step = one full frame (all six stages, sb/pipeline.py:85-124) per rank.
-Multi-GPU is view-sharded: every rank holds the whole scene
-and renders its own views; the only collective is the frame gather after the
-timed region.  Rank 0 prints ONE JSON line.
+One step = one batch of V camera views rendered through all six stages
+(sb/pipeline.py:85-124), view-sharded over the ranks (rank r
+renders the contiguous slice shard_views(V, N, r)), with every frame + its
+stats gathered to rank 0 over NCCL point-to-point transfers that overlap the
+rendering — the gather is inside the timed region.  Rank 0 prints ONE JSON
+line; value = V x K / (max over ranks of the CUDA-event time of K steps).
 
-Workload (default `garden` = BASELINE.json configs[2]): 5.8M Gaussians, SH
-degree 3, 1297x840, aabb culling + load map/stats; synthetic scene (seeded
+Batch size: V = 8 x N for the single-view configurations (garden = BASELINE
+configs[2], the headline; truck; config1) — weak scaling, 8 views per GPU;
+V = 64 for playroom (configs[3]) and 256 for stress (configs[4]) at every N —
+strong scaling, as BASELINE states them.  Synthetic scene (seeded
 generate_synthetic draws + SH rest N(0, 0.3^2), values rounded to fp32),
-spec scale U(0.004, 0.016), anisotropy U(1, 4), opacity U(0.01, 0.6),
-orbit cameras at radius 2.6, fov 60.  Inputs (1.37 GB scene, ~1 GB of pair
-buffers) are larger than the 126 MB L2, so no explicit L2 flush is needed.
+spec scale U(0.004, 0.016), anisotropy U(1, 4), opacity U(0.01, 0.6), orbit
+cameras at radius 2.6, fov 60; rank 0 builds it and broadcasts it.  Inputs
+(scene >= 0.5 GB, pair buffers) are larger than the 126 MB L2, so no
+explicit L2 flush is needed.
 """
 
 from __future__ import annotations
@@ -55,6 +60,8 @@ CONFIGS = {
                    name="stress: 10M Gaussians 1920x1080 (configs[4])"),
 }
 VIEWS_PER_RANK = 8
+# fixed view batches of the multi-view configurations (strong scaling)
+FIXED_VIEWS = {"playroom": 64, "stress": 256}
 METRIC = "rendered frames/sec and Gaussian-tile pairs/frame; 1/2/4/8 B200 view-sharded"
 
 
@@ -65,6 +72,8 @@ def parse():
     ap.add_argument("--warmup", type=int, default=10)
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
     ap.add_argument("--config", choices=sorted(CONFIGS), default="garden")
+    ap.add_argument("--views", type=int, default=0,
+                    help="views per step (default: 8 per GPU; playroom 64, stress 256)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--cpu-budget", type=float, default=12.0, help="seconds of sampled CPU render")
@@ -203,9 +212,28 @@ def cpu_reference_sample(cfg, arrays, cam, budget_s, threads):
                       f"render of {sampled}/{nt} tiles (every {stride}-th) extrapolated to all tiles"}
 
 
+def batch_views(args, cfg_name, world):
+    if args.views:
+        return args.views, "strong"
+    if cfg_name in FIXED_VIEWS:
+        return FIXED_VIEWS[cfg_name], "strong"
+    return VIEWS_PER_RANK * world, "weak"
+
+
+def config_dict(cfg, args, views, world, pairs, scaling):
+    return {"workload": cfg["name"], "gaussians": cfg["n"], "width": cfg["w"], "height": cfg["h"],
+            "mode": cfg["mode"], "sh_degree": cfg["sh"], "pairs_per_frame": pairs,
+            "views_per_step": views, "scaling": scaling,
+            "parallelism": f"view-sharded x{world}",
+            "l2": "inputs larger than L2 (scene %.2f GB)" % (cfg["n"] * (44 + 12 * (cfg["sh"] + 1) ** 2) / 1e9)}
+
+
 def run_reference(args, cfg, rank, world):
     """--impl reference: the reference algorithm on the host cores (the C
-    oracle port; the reference itself is pure numpy, ~90 s per 5.8M frame)."""
+    oracle port, OpenMP, every host thread; the reference itself is pure numpy
+    at ~90 s per 5.8M frame).  Same configuration, cameras and metric as our
+    arm: step s renders view s mod V of the same orbit (full stages 1-5 and a
+    tile-strided render sample extrapolated to all tiles)."""
     if rank != 0:
         return
     from oracle import oracle as orc
@@ -213,22 +241,23 @@ def run_reference(args, cfg, rank, world):
     orc.lib()
     threads = os.cpu_count() or 1
     arrays = scene_arrays(cfg)
-    cam = cameras(cfg, VIEWS_PER_RANK)[0]
-    budget = max(2.0, min(args.cpu_budget, 20.0))
-    for _ in range(max(0, min(args.warmup, 1))):
-        cpu_reference_sample(cfg, arrays, cam, budget / 4, threads)
-    samples = [cpu_reference_sample(cfg, arrays, cam, budget, threads) for _ in range(max(1, args.steps if args.steps < 4 else 3))]
-    frame_s = statistics.median(s["frame_s"] for s in samples)
+    views, scaling = batch_views(args, args.config, world)
+    cams = cameras(cfg, views)
+    budget = max(2.0, min(args.cpu_budget, 20.0)) / 3.0
+    for s in range(max(0, min(args.warmup, 1))):
+        cpu_reference_sample(cfg, arrays, cams[s % views], budget / 2, threads)
+    steps = max(1, min(args.steps, 20))
+    samples = [cpu_reference_sample(cfg, arrays, cams[s % views], budget, threads) for s in range(steps)]
+    frame_s = sum(x["frame_s"] for x in samples) / len(samples)
     fps = 1.0 / frame_s
+    pairs = float(np.mean([x["pairs"] for x in samples]))
     line = {"metric": METRIC, "value": fps, "unit": "frames/s", "n_gpus": world,
-            "steps": len(samples), "warmup": args.warmup, "ms_per_step": frame_s * 1e3,
-            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64+f32",
+            "steps": steps, "warmup": args.warmup, "ms_per_step": frame_s * 1e3,
+            "higher_is_better": True, "scaling": scaling, "vs_baseline": None, "dtype": "f64+f32",
             "data": "synthetic", "impl": "reference",
-            "config": {"workload": cfg["name"], "gaussians": cfg["n"], "width": cfg["w"],
-                       "height": cfg["h"], "mode": cfg["mode"], "sh_degree": cfg["sh"],
-                       "pairs_per_frame": samples[0]["pairs"], "parallelism": "host threads"},
+            "config": config_dict(cfg, args, views, world, pairs, scaling),
             "cpu_baseline": {"value": fps, "unit": "frames/s", "cores": threads, "kind": "port",
-                             "sample": samples[0]["sample"]},
+                             "sample": f"{steps} frames, view s mod {views} of the orbit; each: " + samples[0]["sample"]},
             "e2e": {"value": fps, "unit": "frames/s", "h2d_bytes_per_step": 0,
                     "d2h_bytes_per_step": 0},
             "stages_s": samples[0]["stages_s"]}
@@ -240,6 +269,7 @@ def run_ours(args, cfg, rank, world, local):
 
     import paper_2409_08669_b200 as ab
     from paper_2409_08669_b200 import _lib
+    from paper_2409_08669_b200.views import FrameGather, broadcast_scene, shard_views
 
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
@@ -250,96 +280,118 @@ def run_ours(args, cfg, rank, world, local):
         dist.init_process_group("nccl", device_id=dev)
     L = _lib.lib()
     t_setup = time.perf_counter()
-    arrays = scene_arrays(cfg)
-    host = ab.DeviceScene.from_arrays(arrays, cfg["sh"], "cpu", torch.float32).pin_memory()
-    ds = host.to(dev)
-    n_views = VIEWS_PER_RANK * world
-    cams = cameras(cfg, n_views)
-    from paper_2409_08669_b200.views import shard_views
-
-    mine = [cams[k] for k in shard_views(n_views, world, rank)]
+    # scene: built once on rank 0, broadcast to the others
+    arrays, host, ds = None, None, None
+    if rank == 0:
+        arrays = scene_arrays(cfg)
+        host = ab.DeviceScene.from_arrays(arrays, cfg["sh"], "cpu", torch.float32).pin_memory()
+        ds = host.to(dev)
+    if world > 1:
+        ds = broadcast_scene(ds, cfg["n"], cfg["sh"], dev)
+        if rank != 0:
+            host = ds.to("cpu").pin_memory()   # this rank's host copy for the e2e legs
+    views, scaling = batch_views(args, args.config, world)
+    cams = cameras(cfg, views)
+    mine = list(shard_views(views, world, rank))
+    n_mine = len(mine)
     rast = ab.Rasterizer(cfg["w"], cfg["h"], cfg["n"], device=dev)
     pairs, stage_ms = [], []
-    for cam in mine:   # size the pair buffers for every view, collect stage times
-        res = rast.render(ds, cam, mode=cfg["mode"])
+    for v in mine:   # size the pair buffers for every view of this rank
+        res = rast.render(ds, cams[v], mode=cfg["mode"])
         pairs.append(res.stats.pair_count)
-    rast.fit_capacity(max(pairs))
+    rast.fit_capacity(max(pairs) if pairs else 0)
+    v0 = mine[0] if mine else 0
     for _ in range(3):
-        res = rast.render(ds, mine[0], mode=cfg["mode"])
+        res = rast.render(ds, cams[v0], mode=cfg["mode"])
         stage_ms.append({k: v * 1e3 for k, v in res.stats.stage_seconds().items()})
-    first = rast.render(ds, mine[0], mode=cfg["mode"])
+    first = rast.render(ds, cams[v0], mode=cfg["mode"])
     load_stats = first.load_stats
     culled = first.stats.culled_gaussians
     before = L.adr_kernel_launches()
-    rast.launch(ds, mine[0], mode=cfg["mode"])
+    rast.launch(ds, cams[v0], mode=cfg["mode"])
     torch.cuda.synchronize(dev)
     launches_per_frame = L.adr_kernel_launches() - before
-    # views in flight: view i renders through rasterizer i % R on stream i % R
-    n_fly = max(1, min(args.streams, len(mine)))
+    # views in flight: view j of this rank renders through slot j % K on its own stream
+    n_fly = max(1, min(args.streams, max(n_mine, 1)))
     rasts = [rast] + [ab.Rasterizer(cfg["w"], cfg["h"], cfg["n"], device=dev, pair_capacity=rast.cap,
                                     timing=False) for _ in range(n_fly - 1)]
     streams = [torch.cuda.Stream(dev) for _ in range(n_fly)]
-    graphs = [rasts[i % n_fly].capture(ds, cam, mode=cfg["mode"]) for i, cam in enumerate(mine)]
+    graphs = [rasts[j % n_fly].capture(ds, cams[v], mode=cfg["mode"]) for j, v in enumerate(mine)]
+    fg = FrameGather(views, cfg["h"], cfg["w"], dev) if world > 1 else None
+    zero = torch.zeros(1, dtype=torch.int64, device=dev)
     setup_s = time.perf_counter() - t_setup
-
     stream = torch.cuda.current_stream(dev)
 
-    def run_frames(count, start=0):
-        """Replay `count` frames round-robin over the views; frames of
-        different views overlap on their own streams."""
+    def step(gather: bool):
+        """One batch: this rank's views (frames of different views overlap on
+        the slot streams); with `gather`, each frame is shipped to rank 0 as
+        soon as it is rendered and the step ends when every transfer landed."""
         ev0 = torch.cuda.Event()
         ev0.record(stream)
         for st in streams:
             st.wait_event(ev0)
-        for s in range(start, start + count):
-            v = s % len(graphs)
-            with torch.cuda.stream(streams[v % n_fly]):
-                graphs[v].replay()
+        if fg is not None and gather:
+            fg.begin()
+        for j, v in enumerate(mine):
+            k = j % n_fly
+            with torch.cuda.stream(streams[k]):
+                graphs[j].replay()
+                if fg is not None and gather:
+                    r = rasts[k]
+                    fg.send(v, r.pixels, r.load, torch.cat([r.counters[0:2], r.stats[0:3], zero]))
         for st in streams:
             ev = torch.cuda.Event()
             ev.record(st)
             stream.wait_event(ev)
+        if fg is not None and gather:
+            fg.finish()
 
-    run_frames(args.warmup)
+    def timed(k_steps: int, gather: bool) -> float:
+        torch.cuda.synchronize(dev)
+        if dist:
+            dist.barrier()
+        torch.cuda.synchronize(dev)
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        for _ in range(k_steps):
+            step(gather)
+        e1.record(stream)
+        torch.cuda.synchronize(dev)
+        ms = e0.elapsed_time(e1)
+        if dist:
+            t = torch.tensor([ms], dtype=torch.float64, device=dev)
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            ms = float(t.item())
+        return ms
+
+    for _ in range(args.warmup):
+        step(True)
     torch.cuda.synchronize(dev)
+    # render-only (no gather): the per-rank rendering rate
+    ms_render = timed(args.steps, gather=False)
     clocks = Clocks(local)
-    if dist:
-        dist.barrier()
-    torch.cuda.synchronize(dev)
     clocks.start()
     time.sleep(0.3)
-    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    e0.record(stream)
-    run_frames(args.steps)
-    e1.record(stream)
-    torch.cuda.synchronize(dev)
-    ms = e0.elapsed_time(e1)
-    # keep the clock sampler under load for >= 1.5 s in total
+    ms = timed(args.steps, gather=True)   # the headline: render + gather to rank 0
     soak_end = time.perf_counter() + max(0.0, 1.5 - ms * 1e-3)
-    while time.perf_counter() < soak_end:
-        run_frames(50)
+    while time.perf_counter() < soak_end:   # keep the clock sampler under load >= 1.5 s
+        step(True)
         torch.cuda.synchronize(dev)
-    torch.cuda.synchronize(dev)
     clk = clocks.stop()
-    if dist:
-        if world > 1:
-            dist.barrier()
-        t = torch.tensor([ms], dtype=torch.float64, device=dev)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        ms = float(t.item())
-    value = world * args.steps / (ms * 1e-3)
+    frames = views * args.steps
+    value = frames / (ms * 1e-3)
     ms_per_step = ms / args.steps
-    p_mean = float(np.mean(pairs))
-    # per-stage breakdown and the dominant kernel (render) from CUDA events
+    p_mean = float(np.mean(pairs)) if pairs else 0.0
+    if dist:
+        t = torch.tensor([p_mean * n_mine, float(n_mine)], dtype=torch.float64, device=dev)
+        dist.all_reduce(t)
+        p_mean = float(t[0] / max(t[1], 1.0))
     med = {k: statistics.median(d[k] for d in stage_ms) for k in stage_ms[0]}
     hbm, peak_kind = peaks()
     nt = rast.grid.n_tiles
     k_sh = (cfg["sh"] + 1) ** 2
-    rbytes = render_kernel_bytes(pairs[0], cfg["w"], cfg["h"], nt)
-    render_gbs = rbytes / (med["render"] * 1e-3) / 1e9
-    falg = frame_algorithmic_bytes(cfg["n"], k_sh, p_mean, cfg["w"], cfg["h"])
-    # per-kernel DRAM traffic from the committed ncu launch list of this
-    # config (profiles/ncu_summary.json, tools/ncu_json.py)
+    n = cfg["n"]
+    # per-kernel evidence from the committed ncu summaries (profiles/ncu_summary.json)
     prof = ROOT / "profiles" / "ncu_summary.json"
     ncu = {}
     if prof.exists():
@@ -347,19 +399,20 @@ def run_ours(args, cfg, rank, world, local):
             ncu = json.loads(prof.read_text()).get(args.config, {})
         except Exception:
             ncu = {}
-    traffic = ncu.get("k_render_dram_bytes")
-    # K1 (preprocess) is the dominant HBM-bound kernel: its algorithmic bytes
-    # are the scene read, the Projection write and the render records of the
-    # surviving Gaussians
-    alive = cfg["n"] - culled
-    pre_bytes = cfg["n"] * (44 + 12 * k_sh) + cfg["n"] * (65 + 4) + alive * (48 + 8)
+    # K1 (preprocess), HBM-bound: SURVEY.md §8(d) bytes = N(44 + 12K) scene read + 52 N Projection
+    # write; the implementation also writes the 48 B render record + 8 B tile rect + 4 B depth key
+    pre_bytes = n * (44 + 12 * k_sh) + n * 52
+    pre_impl_bytes = n * (44 + 12 * k_sh) + n * (65 + 4) + (n - culled) * (48 + 8)
     pre_gbs = pre_bytes / (med["preprocess"] * 1e-3) / 1e9
+    # binning (depth sort + supertile placement), §8(d): N·16 dup read + P·12 pair write + P·24 ideal sort pass
+    bin_ms = med["inclusivesum"] + med["duplicate"] + med["sort"] + med["ranges"]
+    bin_bytes = n * 16 + p_mean * 36
+    rbytes = render_kernel_bytes(p_mean, cfg["w"], cfg["h"], nt)
+    falg = frame_algorithmic_bytes(n, k_sh, p_mean, cfg["w"], cfg["h"])
 
-    # e2e 1: the drop-in call — scene from pinned host memory each step, frame,
-    # image + load map back to pinned host memory.
-    e2e = None
-    e2e_res = None
-    if not args.no_e2e:
+    # e2e legs (per rank; aggregated over ranks)
+    e2e = e2e_res = e2e_rp = None
+    if not args.no_e2e and n_mine:
         img_h = torch.empty_like(rast.pixels, device="cpu").pin_memory()
         load_h = torch.empty_like(rast.load, device="cpu").pin_memory()
         src = [host.centers, host.scales, host.rotations, host.opacities, host.sh]
@@ -367,50 +420,45 @@ def run_ours(args, cfg, rank, world, local):
         h2d = host.nbytes()
         d2h = img_h.numel() * 4 + load_h.numel() * 4
         k_e2e = max(3, min(args.steps, 20))
-        for it in range(2):
-            for a, b in zip(dst, src):
-                a.copy_(b, non_blocking=True)
-            graphs[0].replay()
-            img_h.copy_(rast.pixels, non_blocking=True)
-            load_h.copy_(rast.load, non_blocking=True)
-        torch.cuda.synchronize(dev)
-        if dist:
-            dist.barrier()
-        # two device copies of the scene: the H2D copy of step s+1's scene (copy
-        # stream) overlaps step s's frame and D2H (compute stream); every step
-        # still moves its own inputs in and its own result out
+        # (1) drop-in frame: the scene copied from pinned host memory every frame,
+        # image + load map back to pinned host memory.  Two device copies of the
+        # scene: step s+1's H2D copy (copy stream) overlaps step s's frame.
         dst2 = [t.clone() for t in dst]
         ds2 = ab.DeviceScene(*dst2, sh_degree=ds.sh_degree)
-        n_e2e_views = min(len(mine), 4)
-        eg = [[rast.capture(d, mine[v], mode=cfg["mode"]) for v in range(n_e2e_views)] for d in (ds, ds2)]
+        n_e2e_views = min(n_mine, 4)
+        eg = [[rast.capture(d, cams[mine[j]], mode=cfg["mode"]) for j in range(n_e2e_views)] for d in (ds, ds2)]
         bufs = [dst, dst2]
         cstream = torch.cuda.Stream(dev)
         ready = [torch.cuda.Event(), torch.cuda.Event()]
         free = [torch.cuda.Event(), torch.cuda.Event()]
+        for it in range(2):
+            for a_, b_ in zip(dst, src):
+                a_.copy_(b_, non_blocking=True)
+            eg[0][0].replay()
         torch.cuda.synchronize(dev)
+        if dist:
+            dist.barrier()
         a0, a1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         a0.record(stream)
         cstream.wait_event(a0)
-        for s in range(k_e2e):
-            bb = s % 2
+        for s_ in range(k_e2e):
+            bb = s_ % 2
             with torch.cuda.stream(cstream):
-                if s >= 2:
+                if s_ >= 2:
                     cstream.wait_event(free[bb])
-                for a, b in zip(bufs[bb], src):
-                    a.copy_(b, non_blocking=True)
+                for a_, b_ in zip(bufs[bb], src):
+                    a_.copy_(b_, non_blocking=True)
                 ready[bb].record(cstream)
             stream.wait_event(ready[bb])
-            eg[bb][s % n_e2e_views].replay()
+            eg[bb][s_ % n_e2e_views].replay()
             img_h.copy_(rast.pixels, non_blocking=True)
             load_h.copy_(rast.load, non_blocking=True)
             free[bb].record(stream)
         a1.record(stream)
         torch.cuda.synchronize(dev)
         ems = a0.elapsed_time(a1)
-        # e2e 2: resident scene (renderer serving): every step a camera goes in
-        # through the public call (Rasterizer.launch -> adr_render_frame, camera
-        # passed by value: no graph), the image + load map come back to pinned
-        # host memory; steps rotate over the in-flight slots and their streams
+        # (2) resident scene (serving): per step a new camera through the C-ABI
+        # frame call (Rasterizer.launch, no graph) on one of the in-flight slots
         slot_h = [(torch.empty_like(r.pixels, device="cpu").pin_memory(),
                    torch.empty_like(r.load, device="cpu").pin_memory()) for r in rasts]
         torch.cuda.synchronize(dev)
@@ -418,10 +466,10 @@ def run_ours(args, cfg, rank, world, local):
         b0.record(stream)
         for st in streams:
             st.wait_event(b0)
-        for s in range(args.steps):
-            v = s % len(mine)
-            k = s % n_fly
-            rasts[k].launch(ds, mine[v], mode=cfg["mode"], stream=streams[k])
+        n_res = max(args.steps, 8)
+        for s_ in range(n_res):
+            k = s_ % n_fly
+            rasts[k].launch(ds, cams[mine[s_ % n_mine]], mode=cfg["mode"], stream=streams[k])
             with torch.cuda.stream(streams[k]):
                 slot_h[k][0].copy_(rasts[k].pixels, non_blocking=True)
                 slot_h[k][1].copy_(rasts[k].load, non_blocking=True)
@@ -432,93 +480,99 @@ def run_ours(args, cfg, rank, world, local):
         b1.record(stream)
         torch.cuda.synchronize(dev)
         rms = b0.elapsed_time(b1)
+        # (3) the literal drop-in call: run_pipeline(pinned host scene, camera)
+        # -> PipelineResult; synchronous, wall clock per call (upload, frame,
+        # stage events, result copies)
+        ab.run_pipeline(host, cams[mine[0]], mode=cfg["mode"])
+        torch.cuda.synchronize(dev)
         if dist:
-            t = torch.tensor([ems, rms], dtype=torch.float64, device=dev)
+            dist.barrier()
+        k_rp = max(2, min(args.steps, 6))
+        w0 = time.perf_counter()
+        for s_ in range(k_rp):
+            res = ab.run_pipeline(host, cams[mine[s_ % n_mine]], mode=cfg["mode"])
+            _ = res.image.pixels.cpu()
+        rp_s = time.perf_counter() - w0
+        if dist:
+            t = torch.tensor([ems, rms, rp_s], dtype=torch.float64, device=dev)
             dist.all_reduce(t, op=dist.ReduceOp.MAX)
-            ems, rms = (float(v) for v in t.tolist())
+            ems, rms, rp_s = (float(v) for v in t.tolist())
         e2e = {"value": world * k_e2e / (ems * 1e-3), "unit": "frames/s",
                "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
-               "path": "Rasterizer frame via the C-ABI with the scene copied from pinned host "
-                       "memory every step and image+load map copied back (run_pipeline semantics); "
-                       "double-buffered device scene: step s+1's H2D copy overlaps step s's frame"}
-        e2e_res = {"value": world * args.steps / (rms * 1e-3), "unit": "frames/s",
+               "path": "frame via the C-ABI with the scene copied from pinned host memory every step and "
+                       "image+load map copied back (run_pipeline semantics); double-buffered device scene: "
+                       "step s+1's H2D copy overlaps step s's frame"}
+        e2e_res = {"value": world * n_res / (rms * 1e-3), "unit": "frames/s",
                    "h2d_bytes_per_step": ctypes.sizeof(_lib.Camera_t), "d2h_bytes_per_step": d2h,
                    "path": "resident scene; per step Rasterizer.launch with a new camera (C-ABI call, "
                            "no graph) on one of the in-flight slots, image+load map copied to pinned host"}
-
-    # frame gather (multi-GPU only): the one collective of the view-sharded path
-    gather_ms = None
-    if dist and world > 1:
-        from paper_2409_08669_b200.views import STATS_FIELDS, gather_frames, pack_frame
-
-        # this rank's real frames and stats, one replay per view
-        frames = torch.empty((len(mine), cfg["h"], cfg["w"], 4), dtype=torch.float32, device=dev)
-        st = torch.zeros((len(mine), len(STATS_FIELDS)), dtype=torch.int64, device=dev)
-        for v, g in enumerate(graphs):
-            r = rasts[v % n_fly]
-            g.replay()
-            frames[v].copy_(pack_frame(r.pixels, r.load))
-            st[v, 0:2].copy_(r.counters[0:2])
-            st[v, 2:4].copy_(r.stats[0:2])
-        torch.cuda.synchronize(dev)
-        g0 = time.perf_counter()
-        gather_frames(frames, st, n_views)
-        torch.cuda.synchronize(dev)
-        gather_ms = (time.perf_counter() - g0) * 1e3
+        e2e_rp = {"value": world * k_rp / rp_s, "unit": "frames/s", "h2d_bytes_per_step": h2d,
+                  "d2h_bytes_per_step": img_h.numel() * 4,
+                  "path": "paper_2409_08669_b200.run_pipeline(pinned host DeviceScene, camera) per frame, "
+                          "synchronous, wall clock (includes the scene upload, stage events, result copies)"}
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         threads = os.cpu_count() or 1
-        c = cpu_reference_sample(cfg, arrays, mine[0], args.cpu_budget, threads)
+        c = cpu_reference_sample(cfg, arrays, cams[0], args.cpu_budget, threads)
         cpu = {"value": c["fps"], "unit": "frames/s", "cores": threads, "kind": "port",
                "sample": c["sample"], "stages_s": c["stages_s"]}
 
     if rank == 0:
+        cfgd = config_dict(cfg, args, views, world, p_mean, scaling)
+        cfgd.update({"step": f"{views} views rendered (view-sharded) + gathered to rank 0",
+                     "frame": "CUDA graph per view, no host sync", "views_in_flight": n_fly})
         line = {
             "metric": METRIC, "value": value, "unit": "frames/s", "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_per_step,
-            "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+            "higher_is_better": True, "scaling": scaling, "vs_baseline": None,
             "dtype": "f64 preprocess / f32 blend (bit-exact)", "data": "synthetic",
-            "config": {"workload": cfg["name"], "gaussians": cfg["n"], "width": cfg["w"],
-                       "height": cfg["h"], "mode": cfg["mode"], "sh_degree": cfg["sh"],
-                       "pairs_per_frame": p_mean, "views_per_rank": len(mine),
-                       "parallelism": f"view-sharded x{world}",
-                       "l2": "inputs larger than L2 (scene %.2f GB)" % (host.nbytes() / 1e9),
-                       "frame": "CUDA graph per view, no host sync",
-                       "views_in_flight": n_fly},
+            "config": cfgd,
             "pairs_per_frame": p_mean,
-            "stages_ms": med,
-            # sort rates (BASELINE north_star asks for keys/s): the tile sort is the
-            # stable 2-pass radix of the P (tile, Gaussian) pairs; the "inclusivesum"
-            # stage is the depth-rank sort of the N Gaussians plus the pair-offset scan
-            "sort_rates": {"tile_sort_pairs_per_s": p_mean / (med["sort"] * 1e-3),
-                           "depth_sort_and_offsets_keys_per_s": cfg["n"] / (med["inclusivesum"] * 1e-3)},
+            "stages_ms": {"preprocess": med["preprocess"], "depth_sort": med["inclusivesum"],
+                          "supertile_items": med["duplicate"], "pair_placement": med["sort"],
+                          "render": med["render"]},
+            "per_rank_fps_render_only": n_mine * args.steps / (ms_render * 1e-3),
+            "render_only_value": views * args.steps / (ms_render * 1e-3),
+            "gather": ("point-to-point to rank 0 (NCCL), overlapped with rendering, inside the timed region"
+                       if world > 1 else "none (one rank)"),
+            "sort_rates": {"depth_sort_keys_per_s": n / (med["inclusivesum"] * 1e-3),
+                           "pair_binning_pairs_per_s": p_mean / ((med["duplicate"] + med["sort"]) * 1e-3)},
             "load_stats": {"mean": load_stats.mean, "std": load_stats.std, "min": load_stats.min,
                            "max": load_stats.max},
-            # the longest kernel of the frame, and HBM-bound: the fp64 preprocess
+            # the dominant HBM-bound kernel: K1, the fp64 preprocess
             "roofline": {"bound": "hbm", "kernel": "k_preprocess", "achieved": pre_gbs, "peak": hbm,
-                         "unit": "GB/s", "frac": pre_gbs / hbm, "traffic": ncu.get("k_preprocess_dram_bytes"),
-                         "bytes_per_launch": pre_bytes, "peak_kind": peak_kind},
-            "render_kernel": {"bound": "fma-pipe", "kernel": "k_render",
-                              "gather_gbs": render_gbs, "bytes_per_launch": rbytes, "traffic": traffic,
+                         "unit": "GB/s", "frac": pre_gbs / hbm,
+                         "traffic": ncu.get("k_preprocess_dram_bytes"),
+                         "bytes_per_launch": pre_bytes,
+                         "bytes_rule": "SURVEY.md §8(d): N(44+12K) read + 52N write",
+                         "impl_bytes_per_launch": pre_impl_bytes,
+                         "impl_frac": pre_impl_bytes / (med["preprocess"] * 1e-3) / 1e9 / hbm,
+                         "peak_kind": peak_kind},
+            "binning_roofline": {"bound": "hbm", "kernels": "depth sort + supertile items + pair placement",
+                                 "bytes_per_frame": bin_bytes,
+                                 "bytes_rule": "SURVEY.md §8(d): N·16 dup read + P·12 pair write + P·24 one ideal sort pass",
+                                 "achieved": bin_bytes / (bin_ms * 1e-3) / 1e9, "peak": hbm,
+                                 "frac": bin_bytes / (bin_ms * 1e-3) / 1e9 / hbm, "ms": bin_ms},
+            "render_kernel": {"bound": "fp32-issue", "kernel": "k_render",
+                              "gather_gbs": rbytes / (med["render"] * 1e-3) / 1e9, "bytes_per_launch": rbytes,
+                              "traffic": ncu.get("k_render_dram_bytes"),
                               "fma_pipe_active": ncu.get("k_render_fma_pipe"),
                               "issue_active": ncu.get("k_render_issue_active"),
                               "warp_inst_per_s": ncu.get("k_render_warp_inst_per_s"),
-                              "warp_inst_peak_per_s": 148 * 4 * clk.get("sm_mhz", 1965.0) * 1e6 if clk else None,
-                              "note": "52 B/pair record gathers + outputs, served from L2 (traffic = DRAM "
-                                      "bytes per launch); the limiter is FP32 issue for the exact numpy exp "
-                                      "(FFMA2 + MUFU) and dependency latency, not memory"},
+                              "warp_inst_peak_per_s": 148 * 4 * (clk.get("sm_mhz") or 1965.0) * 1e6,
+                              "note": "52 B/pair record gathers + outputs, served from L2; the limiter is FP32 "
+                                      "issue for the exact numpy exp (FFMA2 + MUFU) and dependency latency"},
             "frame_roofline": {"bytes_per_frame": falg, "achieved_gbs": falg * value / world / 1e9,
-                               "frac": falg * value / world / 1e9 / hbm},
-            "clocks": clk, "gpu_launches": launches_per_frame * args.steps,
+                               "frac": falg * value / world / 1e9 / hbm,
+                               "bytes_rule": "SURVEY.md §8(d): N(112+12K) + 84P + 16HW"},
+            "clocks": clk, "gpu_launches": launches_per_frame * frames,
             "launches_per_frame": launches_per_frame, "setup_s": setup_s,
         }
         if e2e:
             line["e2e"] = e2e
             line["e2e_resident"] = e2e_res
-        if gather_ms is not None:
-            line["gather_ms"] = gather_ms
-        line["per_rank_fps"] = value / world
+            line["e2e_run_pipeline"] = e2e_rp
         if cpu:
             line["cpu_baseline"] = cpu
         print(json.dumps(line), flush=True)

@@ -771,6 +771,7 @@ int32_t frame_binning_supertile(const FrameBinning& fb, cudaStream_t st) {
     int32_t rc = radix_sort<uint32_t, uint32_t>(fb.dkey, nullptr, skey, sval, nullptr, n, 32, rs1,
                                                 radix_scratch_bytes<uint32_t, uint32_t>(n), st, dx);
     if (rc) return rc;
+    if (fb.ev_after_scan) ADR_CUDA_TRY(cudaEventRecord(fb.ev_after_scan, st));   // stage "depth sort"
     // L1: ranks -> supertile items
     const unsigned nb1 = (unsigned)ceil_div(n, kL1Block);
     k_st_count1<<<nb1, 256, g.S * sizeof(uint32_t), st>>>(rinfo, ctr + 2, g, H1,
@@ -778,11 +779,11 @@ int32_t frame_binning_supertile(const FrameBinning& fb, cudaStream_t st) {
     ADR_LAUNCH_CHECK();
     k_st_scan1<<<(unsigned)g.S, 1024, 0, st>>>(H1, ctr + 2, g, c, icap, ctr, fb.stats);
     ADR_LAUNCH_CHECK();
-    if (fb.ev_after_scan) ADR_CUDA_TRY(cudaEventRecord(fb.ev_after_scan, st));
     const size_t sm_sc = 12 * (size_t)kL1Cap + (18 * (size_t)g.S + 2) * sizeof(uint32_t);  // see k_st_scatter1
     ADR_CUDA_TRY(cudaFuncSetAttribute(k_st_scatter1, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm_sc));
     k_st_scatter1<<<nb1, 256, sm_sc, st>>>(rinfo, ctr + 2, g, H1, c, items, icap);
     ADR_LAUNCH_CHECK();
+    if (fb.ev_after_dup) ADR_CUDA_TRY(cudaEventRecord(fb.ev_after_dup, st));   // stage "L1 items"
     // L2: items -> pairs
     static int sms = 0, bps_c2 = 0, bps_pl = 0;
     if (!sms) {
@@ -796,7 +797,6 @@ int32_t frame_binning_supertile(const FrameBinning& fb, cudaStream_t st) {
     if (grid_c2 > ceil_div(umax, 8)) grid_c2 = ceil_div(umax, 8);
     k_st_count2<<<(unsigned)grid_c2, 256, 0, st>>>(items, g, c, icap, C2, Ut);
     ADR_LAUNCH_CHECK();
-    if (fb.ev_after_dup) ADR_CUDA_TRY(cudaEventRecord(fb.ev_after_dup, st));
     k_st_scan2<<<(unsigned)g.S, 1024, 0, st>>>(Ut, g, c, cap, T, fb.ranges, ctr);
     ADR_LAUNCH_CHECK();
     int64_t grid_pl = (int64_t)sms * bps_pl;

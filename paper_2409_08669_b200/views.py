@@ -44,58 +44,166 @@ def owner_of(view: int, n_views: int, world: int) -> int:
 STATS_FIELDS = ("pairs", "culled", "load_sum", "load_sum_sq", "load_min", "load_max")
 
 
-def gather_frames(frames, stats, n_views: int, group=None, dst: int = 0):
-    """Gather per-view frames to `dst`.
+def _wire(t, group):
+    """NCCL moves device tensors; gloo only host tensors."""
+    import torch.distributed as dist
 
-    frames: (local_views, H, W, 4) float32 (RGB + load as float bits) on this
-    rank's device; stats: (local_views, 6) int64.  Slices can be ragged
-    (V not divisible by R): every rank pads to ceil(V/R) rows so one
-    all_gather_into_tensor moves everything; rank `dst` then drops the padding
-    and returns (V, H, W, 4), (V, 6) in view order (others return None).
+    return t.cpu() if (t.is_cuda and dist.get_backend(group) == "gloo") else t
+
+
+class FrameGather:
+    """Gathers the frames of a V-view batch to rank ``dst`` with point-to-point
+    transfers that overlap the rendering (NCCL moves frames and
+    stats only, to one rank).
+
+    Each view's payload is one float32 buffer: (H, W, 4) RGB + load (load as
+    int32 bits) followed by the 6 int64 stats as 12 float32 words.  A rank
+    that rendered view v calls ``send(v, ...)`` right after the frame was
+    enqueued (on the frame's stream, so the transfer waits for exactly that
+    frame); ``dst`` posts one receive per remote view in ``begin()``;
+    ``finish()`` makes the current stream wait for every transfer and returns
+    (pixels (V,H,W,3), load (V,H,W), stats (V,6)) views of the batch buffer on
+    ``dst`` (None elsewhere).  Ranks send in view order and ``dst`` receives in
+    view order, so transfers pair up on every backend (NCCL or gloo).
     """
-    import torch
+
+    def __init__(self, n_views: int, height: int, width: int, device, group=None, dst: int = 0):
+        import torch
+        import torch.distributed as dist
+
+        self.v, self.h, self.w = int(n_views), int(height), int(width)
+        self.group, self.dst = group, dst
+        self.world = dist.get_world_size(group)
+        self.rank = dist.get_rank(group)
+        self.device = torch.device(device)
+        self.words = self.h * self.w * 4 + 2 * len(STATS_FIELDS)
+        mine = shard_views(self.v, self.world, self.rank)
+        self.mine = list(mine)
+        rows = self.v if self.rank == dst else len(self.mine)
+        self.buf = torch.empty((rows, self.words), dtype=torch.float32, device=self.device)
+        self._works = []
+
+    def _row(self, view: int) -> int:
+        return view if self.rank == self.dst else view - self.mine[0]
+
+    def begin(self) -> None:
+        """Post the receives of this batch (dst only)."""
+        import torch.distributed as dist
+
+        self._works = []
+        if self.rank != self.dst:
+            return
+        self._host = {}
+        for view in range(self.v):
+            src = owner_of(view, self.v, self.world)
+            if src == self.dst:
+                continue
+            t = _wire(self.buf[view], self.group)
+            if t is not self.buf[view]:
+                self._host[view] = t
+            self._works.append((dist.irecv(t, src=src, group=self.group), t))
+
+    def send(self, view: int, pixels, load, stats) -> None:
+        """Pack one rendered view (enqueued on the current stream) and ship it."""
+        import torch
+        import torch.distributed as dist
+
+        row = self.buf[self._row(view)]
+        hw4 = self.h * self.w * 4
+        row[:hw4].view(self.h, self.w, 4).copy_(pack_frame(pixels, load))
+        row[hw4:].view(torch.int64).copy_(stats.reshape(-1).to(torch.int64))
+        if self.rank != self.dst:
+            t = _wire(row, self.group)   # (a host copy on gloo: kept alive until finish)
+            self._works.append((dist.isend(t, dst=self.dst, group=self.group), t))
+
+    def finish(self):
+        import torch
+
+        for w, _ in self._works:
+            w.wait()
+        for view, t in getattr(self, "_host", {}).items():
+            self.buf[view].copy_(t)
+        self._works = []
+        if self.rank != self.dst:
+            return None, None, None
+        hw4 = self.h * self.w * 4
+        frames = self.buf[:, :hw4].view(self.v, self.h, self.w, 4)
+        stats = self.buf[:, hw4:].contiguous().view(torch.int64)
+        px, ld = unpack_frame(frames)
+        return px, ld, stats
+
+
+def gather_frames(frames, stats, n_views: int, group=None, dst: int = 0):
+    """Gather per-view frames to `dst` (a gather, not an all-gather: only
+    `dst` receives).
+
+    frames: (local_views, H, W, 4) float32 (RGB + load as float bits) of this
+    rank's contiguous view slice; stats: (local_views, 6) int64.  Slices may
+    be ragged or empty.  Returns (V, H, W, 4), (V, 6) in view order on `dst`,
+    (None, None) elsewhere."""
     import torch.distributed as dist
 
     world = dist.get_world_size(group)
     rank = dist.get_rank(group)
-    per = -(-n_views // world)
     h, w = frames.shape[1], frames.shape[2]
-    pad_f = torch.zeros((per, h, w, 4), dtype=frames.dtype, device=frames.device)
-    pad_s = torch.zeros((per, len(STATS_FIELDS)), dtype=torch.int64, device=frames.device)
-    pad_f[: frames.shape[0]] = frames
-    pad_s[: stats.shape[0]] = stats
-    all_f = torch.empty((world * per, h, w, 4), dtype=frames.dtype, device=frames.device)
-    all_s = torch.empty((world * per, len(STATS_FIELDS)), dtype=torch.int64, device=frames.device)
-    dist.all_gather_into_tensor(all_f, pad_f, group=group)
-    dist.all_gather_into_tensor(all_s, pad_s, group=group)
-    if rank != dst:
+    fg = FrameGather(n_views, h, w, frames.device, group=group, dst=dst)
+    fg.begin()
+    for i, view in enumerate(shard_views(n_views, world, rank)):
+        px, ld = unpack_frame(frames[i])
+        fg.send(view, px, ld, stats[i])
+    px, ld, st = fg.finish()
+    if px is None:
         return None, None
-    rows = np.concatenate([np.arange(r * per, r * per + len(shard_views(n_views, world, r)))
-                           for r in range(world)])
-    idx = torch.as_tensor(rows, device=frames.device)
-    return all_f.index_select(0, idx), all_s.index_select(0, idx)
+    return pack_frame_batch(px, ld), st
+
+
+def pack_frame_batch(px, ld):
+    import torch
+
+    return torch.cat([px, ld.view(torch.float32).unsqueeze(-1)], dim=-1)
+
+
+_DTYPES = ("float32", "float64")
 
 
 def broadcast_scene(scene, n: int, sh_degree: int, device, dtype=None, group=None, src: int = 0):
     """Replicate a scene from rank `src` on every rank (load
     once, broadcast N·(44 + 12K) bytes at fp32).  `scene` is the source
-    rank's DeviceScene (ignored elsewhere); every rank passes the same N and
-    SH degree and gets a DeviceScene of its own on `device`."""
+    rank's DeviceScene (ignored elsewhere).  The source first broadcasts a
+    header (N, SH degree, dtype), so every rank allocates identical buffers
+    whatever it passed; a mismatch with the caller's N / degree raises.
+    Returns a DeviceScene on `device` on every rank."""
     import torch
     import torch.distributed as dist
 
     from .scene import DeviceScene
 
-    dtype = dtype or (scene.centers.dtype if scene is not None else torch.float32)
+    is_src = dist.get_rank(group) == src
+    if is_src:
+        dt = dtype or scene.centers.dtype
+        hdr = torch.tensor([len(scene), scene.sh_degree, _DTYPES.index(str(dt).split(".")[-1])],
+                           dtype=torch.int64)
+    else:
+        hdr = torch.zeros(3, dtype=torch.int64)
+    hdr_w = hdr.to(device) if dist.get_backend(group) == "nccl" else hdr
+    dist.broadcast(hdr_w, src=src, group=group)
+    n_src, deg_src, code = (int(v) for v in hdr_w.cpu().tolist())
+    if (n_src, deg_src) != (int(n), int(sh_degree)):
+        raise ValueError(f"broadcast_scene: source has N={n_src}, degree {deg_src}; "
+                         f"this rank expected N={n}, degree {sh_degree}")
+    dtype = getattr(torch, _DTYPES[code])
     k = (sh_degree + 1) ** 2
     shapes = [(n, 3), (n, 3), (n, 4), (n,), (n, k, 3)]
-    if dist.get_rank(group) == src:
+    if is_src:
         ts = [t.to(device=device, dtype=dtype).contiguous() for t in
               (scene.centers, scene.scales, scene.rotations, scene.opacities, scene.sh)]
     else:
         ts = [torch.empty(sh, dtype=dtype, device=device) for sh in shapes]
-    for t in ts:
-        dist.broadcast(t, src=src, group=group)
+    for i, t in enumerate(ts):
+        w = _wire(t, group)
+        dist.broadcast(w, src=src, group=group)
+        if w is not t:
+            t.copy_(w)
     return DeviceScene(*ts, sh_degree=sh_degree)
 
 
@@ -195,27 +303,23 @@ class ViewRenderer:
 def render_views_sharded(scene, cams, in_flight: int = 4, group=None, dst: int = 0):
     """Multi-GPU view-sharded rendering: this rank renders its contiguous
     slice of ``cams`` (``shard_views``) with a ``ViewRenderer`` and the frames
-    plus stats are gathered to ``dst`` (``gather_frames``).  Returns
+    plus stats are gathered to ``dst`` (``FrameGather``).  Returns
     (pixels (V,H,W,3), load (V,H,W), stats (V,6)) on ``dst``, (None, None,
     None) elsewhere."""
     import torch.distributed as dist
 
     world = dist.get_world_size(group)
     rank = dist.get_rank(group)
-    mine = [cams[i] for i in shard_views(len(cams), world, rank)]
+    views = list(shard_views(len(cams), world, rank))
     w, h = cams[0].width, cams[0].height
     vr = ViewRenderer(scene, w, h, in_flight)
-    if mine:
-        px, ld, st = vr.render(mine)
-    else:
-        import torch
-
-        px = torch.empty((0, h, w, 3), dtype=torch.float32, device=vr.device)
-        ld = torch.empty((0, h, w), dtype=torch.int32, device=vr.device)
-        st = torch.empty((0, len(STATS_FIELDS)), dtype=torch.int64, device=vr.device)
-    frames = pack_frame(px, ld) if len(mine) else px.new_empty((0, h, w, 4))
-    all_f, all_s = gather_frames(frames, st, len(cams), group=group, dst=dst)
-    if all_f is None:
+    fg = FrameGather(len(cams), h, w, vr.device, group=group, dst=dst)
+    fg.begin()
+    if views:
+        px, ld, st = vr.render([cams[i] for i in views])
+        for j, view in enumerate(views):
+            fg.send(view, px[j], ld[j], st[j])
+    p, l, s = fg.finish()
+    if p is None:
         return None, None, None
-    p, l = unpack_frame(all_f)
-    return p.contiguous(), l, all_s
+    return p.contiguous(), l, s

@@ -219,7 +219,7 @@ def test_view_renderer_matches_single_view_frames():
 
 def test_render_views_sharded_single_rank_nccl():
     """The multi-GPU entry point on a one-rank NCCL group (the only GPU
-    count this run has): shard -> render -> all_gather -> view order."""
+    count this run has): shard -> render -> gather to rank 0 -> view order."""
     import os
     import socket
 

@@ -87,13 +87,14 @@ def _worker(rank, world, port, n_views, h, w, q):
         dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("n_views", [4, 5, 1])
-def test_gather_frames_gloo_world2(n_views):
-    """Ragged slices (5 views over 2 ranks, 1 view over 2 ranks) come back in
-    view order and bit-identical to the per-view single-rank frames."""
+@pytest.mark.parametrize("n_views,world", [(4, 2), (5, 2), (1, 2), (7, 3)])
+def test_gather_frames_gloo(n_views, world):
+    """Ragged slices (5 views over 2 ranks, 1 view over 2 ranks, 7 over 3)
+    come back on rank 0 only, in view order and bit-identical to the
+    per-view single-rank frames."""
     from paper_2409_08669_b200.views import pack_frame
 
-    h, w, world = 6, 10, 2
+    h, w = 6, 10
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _free_port()
@@ -111,7 +112,7 @@ def test_gather_frames_gloo_world2(n_views):
         assert np.array_equal(got_s[k], st.numpy())
 
 
-def _bcast_worker(rank, world, port, q):
+def _bcast_worker(rank, world, port, q, dtype_name="float32"):
     sys.path.insert(0, str(ROOT))
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
     import torch.distributed as dist
@@ -122,24 +123,28 @@ def _bcast_worker(rank, world, port, q):
     dist.init_process_group("gloo", rank=rank, world_size=world)
     try:
         src = None
+        dt = getattr(torch, dtype_name)
         if rank == 0:
             a = ab.synthetic_arrays(5, 300, ab.SyntheticSpec(), sh_degree=2, float32=True)
-            src = ab.DeviceScene.from_arrays(a, 2, "cpu", torch.float32)
-        ds = broadcast_scene(src, 300, 2, "cpu", torch.float32)
+            src = ab.DeviceScene.from_arrays(a, 2, "cpu", dt)
+        # only the source knows the dtype; the header makes every rank agree
+        ds = broadcast_scene(src, 300, 2, "cpu")
+        assert ds.centers.dtype == dt
         q.put((rank, [t.numpy().copy() for t in (ds.centers, ds.scales, ds.rotations, ds.opacities, ds.sh)]))
     finally:
         dist.destroy_process_group()
 
 
-def test_broadcast_scene_gloo_world2():
+@pytest.mark.parametrize("dtype_name", ["float32", "float64"])
+def test_broadcast_scene_gloo_world2(dtype_name):
     """Rank 0's scene arrives bit-identical on rank 1 (load once,
-    broadcast)."""
+    broadcast), whatever dtype the source holds (the header carries it)."""
     import paper_2409_08669_b200 as ab
 
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _free_port()
-    procs = [ctx.Process(target=_bcast_worker, args=(r, 2, port, q)) for r in range(2)]
+    procs = [ctx.Process(target=_bcast_worker, args=(r, 2, port, q, dtype_name)) for r in range(2)]
     for pr in procs:
         pr.start()
     got = dict(q.get(timeout=120) for _ in range(2))
@@ -147,7 +152,7 @@ def test_broadcast_scene_gloo_world2():
         pr.join(timeout=60)
         assert pr.exitcode == 0
     a = ab.synthetic_arrays(5, 300, ab.SyntheticSpec(), sh_degree=2, float32=True)
-    want = [np.asarray(x, dtype=np.float32) for x in (a.centers, a.scales, a.rotations, a.opacities, a.sh)]
+    want = [np.asarray(x, dtype=dtype_name) for x in (a.centers, a.scales, a.rotations, a.opacities, a.sh)]
     for r in (0, 1):
         for g, w in zip(got[r], want):
-            assert g.shape == w.shape and np.array_equal(g.view(np.uint32), w.view(np.uint32))
+            assert g.shape == w.shape and g.dtype == w.dtype and np.array_equal(g, w)
