@@ -165,6 +165,17 @@ int32_t adr_exp_np_f32(const float* d_x, float* d_y, int64_t n, void* stream);
  * checked, d_result[2] = smallest mismatching bit pattern (all-ones if none). */
 int32_t adr_selftest_exp(uint64_t* d_result, void* stream);
 
+/* Render self-check (test infrastructure, no reference counterpart).  With
+ * enable != 0 the following frames launch the counting instantiation of the
+ * tile blend, which iterates each warp's plain bounding box and counts every
+ * splat the 8x8-quadrant tau-ellipse mask would have skipped although one of
+ * the warp's pixels passes the exact power test (an unsafe removal).
+ * host_out (8 counters, may be NULL) receives the counters accumulated since
+ * the previous call (synchronises the device); the call also resets them.
+ * [2] = warp iterations the mask removes, [6] = batches + 1e9 x unsafe
+ * removals (must stay < 1e9). */
+int32_t adr_render_selfcheck(int32_t enable, unsigned long long* host_out);
+
 /* ----------------------------------------------- brute-force reference path */
 
 /* render_reference (sb/oracle.py:23-78) on the GPU: given a BASELINE-mode

@@ -16,14 +16,16 @@
 
 namespace adr {
 
-#ifdef ADR_RENDER_PROFILE
-// opt-in build (EXTRA_NVFLAGS=-DADR_RENDER_PROFILE, tools/render_profile.py):
-// warp-iteration outcome counters of the blend loop
+// Self-check instantiation (k_render<Src, true>, selected at run time by
+// adr_render_selfcheck): warp-iteration outcome counters of the blend loop,
+// including every quad_mask removal that would have skipped a contributing
+// pixel (must stay 0; tests/test_gpu_parity.py, tools/render_profile.py).
+// The frame path launches the PROF = false instantiation, which has none of it.
 __device__ unsigned long long g_render_prof[8];
-#define RPROF(i, v) rp[i] += (v)
-#else
-#define RPROF(i, v) ((void)0)
-#endif
+#define RPROF(i, v)                          \
+    do {                                     \
+        if constexpr (PROF) rp[i] += (v);    \
+    } while (0)
 
 namespace {
 
@@ -205,7 +207,7 @@ __device__ __forceinline__ void blend_scalar(float fpx, float fpy, const float4&
 // each of them (render.py:110-112).  term > 1 or NaN is k_render_unlit below.
 // nan_flag: null = always check NaN-colour poisoning (stage API); otherwise
 // only when *nan_flag != 0 (the fused frame's count of NaN-colour rows).
-template <class Src>
+template <class Src, bool PROF = false>
 __global__ void __launch_bounds__(kRenderThreads, Src::kMinBlocks)
 k_render(Src src, const int64_t* __restrict__ ranges, int32_t width, int32_t height, int32_t tiles_x, float bg0,
          float bg1, float bg2, float alpha_low, float term, float* __restrict__ pixels, int32_t* __restrict__ load,
@@ -238,9 +240,7 @@ k_render(Src src, const int64_t* __restrict__ ranges, int32_t width, int32_t hei
     // are never written)
     f2 T = pk(in0 ? 1.0f : 0.0f, in1 ? 1.0f : 0.0f), C0 = 0ull, C1 = 0ull, C2 = 0ull;
     int cnt0 = 0, cnt1 = 0;
-#ifdef ADR_RENDER_PROFILE
     unsigned long long rp[8] = {0, 0, 0, 0, 0, 0, 0, 0};
-#endif
 #define DONE0 (lo_of(T) < term)
 #define DONE1 (hi_of(T) < term)
     int64_t stop = end;   // first batch at whose start every pixel was done
@@ -255,22 +255,19 @@ k_render(Src src, const int64_t* __restrict__ ranges, int32_t width, int32_t hei
             sG[i] = r.a;
             sT[i] = make_float4(r.b.x, r.c.y, 0.f, 0.f);
             sW[i] = make_float4(r.b.y, r.b.z, r.b.w, r.c.x);
-#ifdef ADR_RENDER_PROFILE
-            smask[i] = (uint8_t)(quad_mask(r, x_lo, y_lo) | (warp_mask(r, x_lo, y_lo) << 4));
-#else
-            smask[i] = (uint8_t)quad_mask(r, x_lo, y_lo);
-#endif
+            if constexpr (PROF)
+                smask[i] = (uint8_t)(quad_mask(r, x_lo, y_lo) | (warp_mask(r, x_lo, y_lo) << 4));
+            else
+                smask[i] = (uint8_t)quad_mask(r, x_lo, y_lo);
         }
         __syncthreads();
         RPROF(6, 1);
         if (__any_sync(kFull, !(DONE0 && DONE1))) {
             for (int c0 = 0; c0 < nb; c0 += 32) {
-#ifdef ADR_RENDER_PROFILE
+                // PROF: iterate the plain box (bits 4-7) and remember the quadrant mask
                 const uint32_t qm = __ballot_sync(kFull, c0 + lane < nb && ((smask[c0 + lane] >> warp) & 1u));
-                uint32_t m = __ballot_sync(kFull, c0 + lane < nb && ((smask[c0 + lane] >> (4 + warp)) & 1u));
-#else
-                uint32_t m = __ballot_sync(kFull, c0 + lane < nb && ((smask[c0 + lane] >> warp) & 1u));
-#endif
+                uint32_t m = PROF ? __ballot_sync(kFull, c0 + lane < nb && ((smask[c0 + lane] >> (4 + warp)) & 1u))
+                                  : qm;
                 while (m) {
                     const int j = c0 + __ffs(m) - 1;
                     m &= m - 1u;
@@ -306,13 +303,13 @@ k_render(Src src, const int64_t* __restrict__ ranges, int32_t width, int32_t hei
                     RPROF(4, (unsigned)p0 + (unsigned)p1);
                     RPROF(1, __all_sync(kFull, !(p0 || p1)));
                     RPROF(7, __all_sync(kFull, !(p0 || p1)) && __all_sync(kFull, !DONE0 && !DONE1));
-#ifdef ADR_RENDER_PROFILE
-                    // slot 2: iterations quad_mask removes; slot 6 += 1e9 per unsafe removal
-                    if (!((qm >> (j - c0)) & 1u)) {
-                        RPROF(2, lane == 0);
-                        if (__any_sync(kFull, p0 || p1) && lane == 0) rp[6] += 1000000000ull;
+                    if constexpr (PROF) {
+                        // slot 2: iterations quad_mask removes; slot 6 += 1e9 per unsafe removal
+                        if (!((qm >> (j - c0)) & 1u)) {
+                            RPROF(2, lane == 0);
+                            if (__any_sync(kFull, p0 || p1) && lane == 0) rp[6] += 1000000000ull;
+                        }
                     }
-#endif
                     if (!(p0 || p1)) continue;  // both alphas < alpha_low for sure
                     const float4 W = lds_f4<16 * kBatch>(sa);
                     const f2 al = mul2(bc(W.x), exp2_np_fast(pw, K), K);
@@ -339,15 +336,15 @@ k_render(Src src, const int64_t* __restrict__ ranges, int32_t width, int32_t hei
     }
 #undef DONE0
 #undef DONE1
-#ifdef ADR_RENDER_PROFILE
-    // per-warp events (0, 1, 2, 6) counted once per warp; per-pixel sums (3, 4, 5) summed over lanes
-    for (int k = 0; k < 8; ++k) {
-        unsigned long long v = rp[k];
-        if (k == 3 || k == 4 || k == 5)
-            for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(kFull, v, o);
-        if (lane == 0) atomicAdd(&g_render_prof[k], v);
+    if constexpr (PROF) {
+        // per-warp events (0, 1, 2, 6) counted once per warp; per-pixel sums (3, 4, 5) summed over lanes
+        for (int k = 0; k < 8; ++k) {
+            unsigned long long v = rp[k];
+            if (k == 3 || k == 4 || k == 5)
+                for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(kFull, v, o);
+            if (lane == 0) atomicAdd(&g_render_prof[k], v);
+        }
     }
-#endif
     uint32_t poison = 0;
     if (!nan_flag || *nan_flag != 0) {
         // every pixel was done at the start of batch `stop`, not at the start
@@ -527,6 +524,8 @@ int32_t launch_init_stats(adr_load_stats* stats, int32_t* hist, int32_t bins, cu
     return ADR_OK;
 }
 
+static int g_render_selfcheck = 0;
+
 int32_t launch_render(const RenderArgs& a, cudaStream_t st) {
     const int64_t n_tiles = (int64_t)a.tiles_x * a.tiles_y;
     if (n_tiles <= 0) return ADR_OK;
@@ -543,10 +542,10 @@ int32_t launch_render(const RenderArgs& a, cudaStream_t st) {
         k_tile_order<<<1, 1024, 0, st>>>(a.ranges, (int32_t)n_tiles, a.order);
         ADR_LAUNCH_CHECK();
     }
-    k_render<RecSource><<<n_tiles, kRenderThreads, 0, st>>>(src, a.ranges, a.width, a.height, a.tiles_x, a.bg[0],
-                                                            a.bg[1], a.bg[2], a.alpha_low, a.term, a.pixels, a.load,
-                                                            a.stats, a.hist, a.hist_bins, f2k_host(), a.order,
-                                                            a.nan_flag);
+    auto kern = g_render_selfcheck ? k_render<RecSource, true> : k_render<RecSource, false>;
+    kern<<<n_tiles, kRenderThreads, 0, st>>>(src, a.ranges, a.width, a.height, a.tiles_x, a.bg[0], a.bg[1], a.bg[2],
+                                             a.alpha_low, a.term, a.pixels, a.load, a.stats, a.hist, a.hist_bins,
+                                             f2k_host(), a.order, a.nan_flag);
     ADR_LAUNCH_CHECK();
     return ADR_OK;
 }
@@ -573,12 +572,17 @@ int32_t launch_render_proj(const adr_projection& p, const int64_t* gidx, const i
 
 }  // namespace adr
 
-#ifdef ADR_RENDER_PROFILE
-extern "C" int32_t adr_debug_render_profile(unsigned long long* host_out) {
-    cudaDeviceSynchronize();
-    cudaMemcpyFromSymbol(host_out, adr::g_render_prof, sizeof(unsigned long long) * 8);
+extern "C" int32_t adr_render_selfcheck(int32_t enable, unsigned long long* host_out) {
+    // counters: [0] warp iterations, [1] iterations with no pixel passing tau,
+    // [2] iterations quad_mask removed, [3] live pixel visits, [4] pixels passing
+    // tau, [5] contributing pixels, [6] batches + 1e9 x unsafe quad_mask removals,
+    // [7] all-fail iterations with no done pixel
+    if (host_out) {
+        ADR_CUDA_TRY(cudaDeviceSynchronize());
+        ADR_CUDA_TRY(cudaMemcpyFromSymbol(host_out, adr::g_render_prof, sizeof(unsigned long long) * 8));
+    }
     unsigned long long z[8] = {0, 0, 0, 0, 0, 0, 0, 0};
-    cudaMemcpyToSymbol(adr::g_render_prof, z, sizeof(z));
-    return 0;
+    ADR_CUDA_TRY(cudaMemcpyToSymbol(adr::g_render_prof, z, sizeof(z)));
+    adr::g_render_selfcheck = enable ? 1 : 0;
+    return ADR_OK;
 }
-#endif

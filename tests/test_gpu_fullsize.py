@@ -246,3 +246,37 @@ def test_render_views_sharded_single_rank_nccl():
             assert int(st[i, 0]) == res.stats.pair_count
     finally:
         dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("name", ["garden", "truck", "stress"])
+def test_quadrant_mask_never_skips_a_contribution(name):
+    """The render's 8x8-quadrant tau-ellipse mask (csrc/adr_render.cu:
+    quad_mask) is a pure work filter: the self-check instantiation walks the
+    plain bounding box instead and counts every splat the mask would have
+    removed although a pixel of the warp passes the exact power test.  Zero
+    such removals on full-size BASELINE frames (two views each), the mask
+    does remove work, and the frame is bit-identical either way."""
+    import torch
+
+    import paper_2409_08669_b200 as ab
+    from paper_2409_08669_b200 import _lib
+
+    cfg, bench = _cfg(name)
+    ds = ab.DeviceScene.from_arrays(bench.scene_arrays(cfg), cfg["sh"], "cuda", torch.float32)
+    L = _lib.lib()
+    out = (__import__("ctypes").c_ulonglong * 8)()
+    r = ab.Rasterizer(cfg["w"], cfg["h"], cfg["n"])
+    try:
+        for cam in bench.cameras(cfg, 8)[:2]:
+            res = r.render(ds, cam, mode=cfg["mode"])
+            px, ld = res.image.pixels.clone(), res.load_map.counts.clone()
+            _lib.check(L.adr_render_selfcheck(1, None))
+            res2 = r.render(ds, cam, mode=cfg["mode"])
+            _lib.check(L.adr_render_selfcheck(0, out))
+            c = [int(v) for v in out]
+            assert c[6] < 10 ** 9, f"{c[6] // 10 ** 9} unsafe quadrant-mask removals"
+            assert c[2] > 0 and c[0] > c[2]
+            assert torch.equal(res2.image.pixels.view(torch.int32), px.view(torch.int32))
+            assert torch.equal(res2.load_map.counts, ld)
+    finally:
+        L.adr_render_selfcheck(0, None)

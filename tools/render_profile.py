@@ -1,7 +1,7 @@
-"""Warp-iteration outcome counters of k_render for one frame, from a library
-built with EXTRA_NVFLAGS=-DADR_RENDER_PROFILE (pass its path in ADR_LIBRARY):
+"""Warp-iteration outcome counters of k_render for one frame (the counting
+instantiation selected at run time by adr_render_selfcheck):
 
-    ADR_LIBRARY=variants/prof.so python tools/render_profile.py --config garden
+    python tools/render_profile.py --config garden
 """
 
 from __future__ import annotations
@@ -33,10 +33,10 @@ def main():
     rast.fit_capacity(res.stats.pair_count)
     L = _lib.lib()
     out = (ctypes.c_ulonglong * 8)()
-    L.adr_debug_render_profile(out)          # reset
+    L.adr_render_selfcheck(1, None)          # reset, counting instantiation on
     res = rast.render(ds, cam, mode=cfg["mode"])
     torch.cuda.synchronize()
-    L.adr_debug_render_profile(out)
+    L.adr_render_selfcheck(0, out)
     it, tau_fail, alpha_fail, live, ptau, pcontrib, batches, tau_fail_nodone = (int(out[i]) for i in range(8))
     P = res.stats.pair_count
     unsafe, batches = divmod(batches, 1000000000)
