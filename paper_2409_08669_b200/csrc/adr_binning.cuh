@@ -29,6 +29,8 @@ struct FrameBinning {
     int32_t tiles_x = 0, tiles_y = 0;
     const uint32_t* dkey = nullptr;  // stage 1 depth-sort key (all-ones: no pairs)
     const uint2* gpack = nullptr;  // per-Gaussian packed tile rect (stage 1)
+    const uint32_t* kminmax = nullptr;  // per preprocess block: min / max selected depth key (optional)
+    uint32_t* plan_mm = nullptr;        // depth plan (min, max), reset by the preprocess
     uint32_t* order = nullptr;  // scratch: order[rank] = Gaussian index
     int64_t* ranges = nullptr;  // out: (n_tiles, 2)
     uint64_t* keys = nullptr;   // optional out: sorted keys (tile << 32 | depth bits)

@@ -33,6 +33,8 @@ struct FrameLayout {
     uint32_t* order;
     Record* rec;
     uint2* gpack;
+    uint32_t* kminmax;
+    uint32_t* plan_mm;
     uint32_t* tile_order;
     void* binning;
     size_t binning_bytes;
@@ -46,6 +48,8 @@ size_t frame_bytes(int64_t n, int32_t tx, int32_t ty, int64_t cap, FrameLayout* 
     l.order = c.take<uint32_t>(n);
     l.rec = c.take<Record>(n);
     l.gpack = c.take<uint2>(n);
+    l.kminmax = c.take<uint32_t>(2 * ceil_div(n > 0 ? n : 1, 128));
+    l.plan_mm = c.take<uint32_t>(2);
     l.tile_order = c.take<uint32_t>(n_tiles);
     l.binning_bytes = frame_binning_scratch(n, cap, tx, ty);
     l.binning = c.take<char>((int64_t)l.binning_bytes);
@@ -158,6 +162,8 @@ int32_t adr_render_frame(const adr_scene* scene, const adr_camera* cam, int32_t 
     fp.ambiguous = reinterpret_cast<unsigned long long*>(buf->d_counters + 5);
     fp.tiles_x = tx;
     fp.tiles_y = ty;
+    fp.kminmax = supertile_path(n_tiles, tx, ty) ? L.kminmax : nullptr;
+    fp.plan_mm = fp.kminmax ? L.plan_mm : nullptr;
     int32_t rc = launch_preprocess(*scene, *cam, mode, alpha_low, dilation, buf->proj, &fp, st);
     if (rc) return rc;
     if (ev[1]) ADR_CUDA_TRY(cudaEventRecord(ev[1], st));
@@ -173,6 +179,8 @@ int32_t adr_render_frame(const adr_scene* scene, const adr_camera* cam, int32_t 
         fb.dkey = L.dkey;
         fb.order = L.order;
         fb.gpack = L.gpack;
+        fb.kminmax = fp.kminmax;
+        fb.plan_mm = fp.plan_mm;
         fb.ranges = buf->d_ranges;
         fb.keys = buf->d_keys;
         fb.gidx = buf->d_gidx;

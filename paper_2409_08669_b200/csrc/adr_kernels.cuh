@@ -78,6 +78,9 @@ struct FusedPre {
     int64_t* d_m = nullptr;                   // += number of Gaussians with pairs (zeroed)
     unsigned long long* nan_colors = nullptr; // += valid rows with a NaN colour channel
     unsigned long long* ambiguous = nullptr;  // += ceil-ambiguous extents (log fence)
+    uint32_t* kminmax = nullptr;              // per block: min and max depth key of the selected rows
+                                              // ([2 b] = min, [2 b + 1] = max; none: all-ones, 0)
+    uint32_t* plan_mm = nullptr;              // the depth plan's (min, max), reset to (all-ones, 0) here
     int32_t tiles_x = 0, tiles_y = 0;
 };
 

@@ -295,6 +295,30 @@ k_preprocess(const T* __restrict__ centers, const T* __restrict__ scales,
             const int amb = __reduce_add_sync(kFull, (unsigned)ambiguous);
             if (lane == 0 && fused.ambiguous) atomicAdd(fused.ambiguous, (unsigned long long)amb);
         }
+        if (fused.kminmax) {   // the depth sort's key-range plan (adr_supertile.cu)
+            __shared__ uint32_t smm[2 * (kPreBlock / 32)];
+            const uint32_t kmn = __reduce_min_sync(kFull, selected ? dbits : 0xffffffffu);
+            const uint32_t kmx = __reduce_max_sync(kFull, selected ? dbits : 0u);
+            const int wid = threadIdx.x >> 5;
+            if (lane == 0) {
+                smm[2 * wid] = kmn;
+                smm[2 * wid + 1] = kmx;
+            }
+            __syncthreads();
+            if (threadIdx.x == 0 && blockIdx.x == 0 && fused.plan_mm) {
+                fused.plan_mm[0] = 0xffffffffu;
+                fused.plan_mm[1] = 0u;
+            }
+            if (threadIdx.x == 0) {
+                uint32_t a = smm[0], b = smm[1];
+                for (int w = 1; w < kPreBlock / 32; ++w) {
+                    a = smm[2 * w] < a ? smm[2 * w] : a;
+                    b = smm[2 * w + 1] > b ? smm[2 * w + 1] : b;
+                }
+                fused.kminmax[2 * blockIdx.x] = a;
+                fused.kminmax[2 * blockIdx.x + 1] = b;
+            }
+        }
         if (lane == 0) {
             if (culled) atomicAdd(fused.culled, (unsigned long long)__popc(culled));
             if (sb) atomicAdd(reinterpret_cast<unsigned long long*>(fused.d_m), (unsigned long long)__popc(sb));

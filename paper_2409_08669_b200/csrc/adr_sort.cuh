@@ -60,14 +60,97 @@ __device__ __forceinline__ uint32_t digit_peers(uint32_t d) {
     return peers;
 }
 
+// Key-range plan of the fused frame's depth sort.  With kmin = the smallest
+// selected depth key rounded down to a multiple of 256, the keys "fit" when
+// every selected key lies within 2^24 - 1 of kmin.  Then the
+// sort runs on 24-bit keys t = key - kmin (all-ones "no pairs" keys ->
+// 0xFFFFFF, still last): pass 0 sorts the raw low byte (equal to t's, kmin
+// being a multiple of 256), pass 1 transforms as it loads, pass 2 is the last
+// pass and restores key = t + kmin, pass 3's kernels exit at once.  Otherwise
+// the 4 passes run on the raw keys.  Decided on the device, so a frame stays
+// one fixed launch sequence (one CUDA graph); the (min, max) pair is reduced
+// by kPlanBlocks extra blocks of pass 0's upsweep from the preprocess's
+// per-block minima / maxima (the preprocess resets it).
+struct DepthPlan {
+    const uint32_t* plan = nullptr;       // (min, max) selected depth key; reset by the preprocess
+    int pass = 0;
+    uint32_t* plan_out = nullptr;         // pass 0 upsweep: the extra blocks' atomic min / max target
+    const uint32_t* kminmax = nullptr;    // per preprocess block: (min, max) selected key
+    int64_t nkb = 0;                      // number of preprocess blocks
+};
+
+constexpr int kPlanBlocks = 16;           // extra blocks of pass 0's upsweep that reduce the plan
+
+// -> fits (three passes suffice), kmin (the key offset, a multiple of 256)
+__device__ __forceinline__ bool plan_decode(const DepthPlan& dp, uint32_t* kmin) {
+    *kmin = 0;
+    if (!dp.plan) return false;
+    const uint2 mm = *reinterpret_cast<const uint2*>(dp.plan);
+    if (mm.x > mm.y) return true;   // no selected Gaussian: every key is all-ones
+    *kmin = mm.x & ~0xffu;
+    return mm.y - *kmin < 0xffffffu;
+}
+
+__device__ __forceinline__ bool plan_fits(const DepthPlan& dp) {
+    uint32_t k;
+    return plan_decode(dp, &k);
+}
+
+// Pass-1 key transform of a register array of keys, applied after all of
+// them were loaded (a per-key plan test between the loads serialises them).
+template <typename K, int N>
+__device__ __forceinline__ void plan_transform(K (&kr)[N], const DepthPlan& dp) {
+    if constexpr (sizeof(K) == 4) {
+        if (dp.pass != 1 || !dp.plan) return;
+        uint32_t kmin;
+        if (!plan_decode(dp, &kmin)) return;
+#pragma unroll
+        for (int r = 0; r < N; ++r) kr[r] = kr[r] == K(0xffffffffu) ? K(0xffffffu) : K((uint32_t)kr[r] - kmin);
+    }
+}
+
+// A plan block (pass 0 upsweep, the last kPlanBlocks blocks of the grid):
+// min / max over its slice of the preprocess blocks' extrema, merged with
+// two atomics.
+template <int BLOCK>
+__device__ __forceinline__ void plan_reduce(const DepthPlan& dp, int slice) {
+    __shared__ uint32_t smn[BLOCK / 32], smx[BLOCK / 32];
+    uint32_t mn = 0xffffffffu, mx = 0u;
+    for (int64_t b = (int64_t)slice * BLOCK + threadIdx.x; b < dp.nkb; b += (int64_t)kPlanBlocks * BLOCK) {
+        const uint2 v = reinterpret_cast<const uint2*>(dp.kminmax)[b];
+        mn = v.x < mn ? v.x : mn;
+        mx = v.y > mx ? v.y : mx;
+    }
+    mn = __reduce_min_sync(0xffffffffu, mn);
+    mx = __reduce_max_sync(0xffffffffu, mx);
+    if ((threadIdx.x & 31) == 0) {
+        smn[threadIdx.x >> 5] = mn;
+        smx[threadIdx.x >> 5] = mx;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        for (int w = 1; w < BLOCK / 32; ++w) {
+            mn = smn[w] < mn ? smn[w] : mn;
+            mx = smx[w] > mx ? smx[w] : mx;
+        }
+        atomicMin(dp.plan_out, mn);
+        atomicMax(dp.plan_out + 1, mx);
+    }
+}
+
 // Block digit histogram: plain shared-memory atomics (no ranking needed).
 template <typename K, int RB>
 __global__ void __launch_bounds__(kSortBlock)
 radix_upsweep(const K* __restrict__ keys, const int64_t* d_n, int64_t n_static, int bit,
-              uint32_t* __restrict__ hist) {
+              uint32_t* __restrict__ hist, DepthPlan dp = DepthPlan()) {
     constexpr int R = 1 << RB;
     constexpr int kIpt = SortCfg<K>::kIpt;
     __shared__ uint32_t h[R];
+    if (dp.plan_out && blockIdx.x >= gridDim.x - kPlanBlocks) {
+        plan_reduce<kSortBlock>(dp, blockIdx.x - (gridDim.x - kPlanBlocks));
+        return;
+    }
+    if (dp.pass == 3 && plan_fits(dp)) return;
     const int64_t n = live_count(d_n, n_static);
     for (int i = threadIdx.x; i < R; i += kSortBlock) h[i] = 0;
     const int64_t base = (int64_t)blockIdx.x * SortCfg<K>::kTileItems;
@@ -77,20 +160,24 @@ radix_upsweep(const K* __restrict__ keys, const int64_t* d_n, int64_t n_static, 
         const int64_t i = base + (int64_t)r * kSortBlock + threadIdx.x;
         kr[r] = i < n ? keys[i] : K(0);
     }
+    plan_transform(kr, dp);
     __syncthreads();
 #pragma unroll
     for (int r = 0; r < kIpt; ++r) {
         if (base + (int64_t)r * kSortBlock + threadIdx.x < n) atomicAdd(&h[digit_of(kr[r], bit, R - 1)], 1u);
     }
     __syncthreads();
-    for (int d = threadIdx.x; d < R; d += kSortBlock) hist[(int64_t)d * gridDim.x + blockIdx.x] = h[d];
+    const int64_t nbh = dp.plan_out ? gridDim.x - kPlanBlocks : gridDim.x;   // histogram blocks
+    for (int d = threadIdx.x; d < R; d += kSortBlock) hist[(int64_t)d * nbh + blockIdx.x] = h[d];
 }
 
 // Exclusive scan of the digit-major histogram (length R * n_blocks), one
 // decoupled look-back pass.
 template <int IPT>
 __global__ void __launch_bounds__(256)
-scan_u32_exclusive(uint32_t* __restrict__ data, int64_t n, uint64_t* status, unsigned long long* counter) {
+scan_u32_exclusive(uint32_t* __restrict__ data, int64_t n, uint64_t* status, unsigned long long* counter,
+                   DepthPlan dp = DepthPlan()) {
+    if (dp.pass == 3 && plan_fits(dp)) return;
     __shared__ int64_t sbid;
     __shared__ uint64_t sred[33];
     __shared__ uint64_t sexcl;
@@ -129,6 +216,7 @@ struct SortExtra {
     const float* exp_depth = nullptr;
     uint64_t* exp_keys = nullptr;
     bool skip_keys_out = false;   // MODE 1: the exported keys carry the tile ids, no separate copy
+    DepthPlan dp;                 // depth-sort key-range plan (MODE 0 / 3 passes of the fused frame)
     const uint2* gsrc = nullptr;
     uint2* gdst = nullptr;
     uint4* rinfo = nullptr;
@@ -153,6 +241,12 @@ radix_downsweep(const K* __restrict__ keys_in, const V* __restrict__ vals_in, K*
     const int64_t n = live_count(d_n, n_static);
     const int64_t base = (int64_t)blockIdx.x * kTile;
     if (base >= n) return;
+    // depth-sort plan: pass 3 is skipped and pass 2 becomes the last (MODE 3)
+    // pass when the keys fit 24 bits
+    uint32_t kmin = 0;
+    const bool fits = ex.dp.pass >= 2 && plan_decode(ex.dp, &kmin);   // passes 2 and 3 change with it
+    if (ex.dp.pass == 3 && fits) return;
+    const bool as_last = MODE == 3 || (ex.dp.pass == 2 && fits);
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     for (int i = threadIdx.x; i < kSortWarps * R; i += kSortBlock) (&wh[0][0])[i] = 0;
     const int64_t wbase = base + (int64_t)warp * 32 * kIpt;
@@ -164,6 +258,7 @@ radix_downsweep(const K* __restrict__ keys_in, const V* __restrict__ vals_in, K*
         kr[r] = i < n ? keys_in[i] : K(0);
         vr[r] = i < n ? (vals_in ? vals_in[i] : V(i)) : V(0);
     }
+    plan_transform(kr, ex.dp);
     __syncthreads();
     // ranks packed two per register (rank within warp < 32 * kIpt <= 512)
     uint32_t rank2[(kIpt + 1) / 2];
@@ -217,9 +312,11 @@ radix_downsweep(const K* __restrict__ keys_in, const V* __restrict__ vals_in, K*
         const K key = skeys[i];
         const V val = svals[i];
         const int64_t g = goff[digit_of(key, bit, R - 1)] + i;
-        if (MODE == 3) {
+        if (MODE == 3 || (MODE == 0 && as_last)) {
             const uint2 r = __ldg(ex.gsrc + val);
-            ex.rinfo[g] = make_uint4((uint32_t)val, (uint32_t)key, r.x, r.y);
+            uint32_t kk = (uint32_t)key;
+            if (fits) kk = kk == 0xffffffu ? 0xffffffffu : kk + kmin;
+            ex.rinfo[g] = make_uint4((uint32_t)val, kk, r.x, r.y);
         } else if (MODE == 2) {
             vals_out[g] = val;
             ex.gdst[g] = __ldg(ex.gsrc + val);
@@ -259,6 +356,8 @@ int32_t radix_sort(const K* keys_in, const V* vals_in, K* keys_out, V* vals_out,
                    const SortExtra& extra = SortExtra()) {
     if (n_max <= 0) return ADR_OK;
     const int passes = pass_count(end_bit);
+    if (extra.dp.plan && (passes != 4 || sizeof(K) != 4))
+        return fail(ADR_ERR_VALUE, "radix_sort: a depth plan needs 32-bit keys and 4 passes");
     if (passes == 0 && (!vals_in || extra.mode != 0))
         return fail(ADR_ERR_VALUE, "radix_sort: identity values / extras need >= 1 pass");
     if (passes == 0) {
@@ -285,36 +384,43 @@ int32_t radix_sort(const K* keys_in, const V* vals_in, K* keys_out, V* vals_out,
         const bool last = p == passes - 1;
         K* dst_k = to_out ? keys_out : alt_k;
         V* dst_v = to_out ? vals_out : alt_v;
+        SortExtra pex = extra;
+        pex.dp.pass = p;
+        const bool plan_block = p == 0 && extra.dp.plan_out;   // pass 0: one extra upsweep block reduces the plan
+        if (!plan_block) pex.dp.plan_out = nullptr;
         ADR_CUDA_TRY(cudaMemsetAsync(status, 0, sizeof(uint64_t) * (scan_blocks_max + 1), st));
 #define ADR_SORT_PASS(RB)                                                                                     \
     do {                                                                                                      \
-        radix_upsweep<K, RB><<<nb, kSortBlock, 0, st>>>(src_k, d_n, n_max, bit, hist);                        \
+        radix_upsweep<K, RB><<<nb + (plan_block ? kPlanBlocks : 0), kSortBlock, 0, st>>>(src_k, d_n, n_max,   \
+                                                                                          bit, hist,          \
+                                                                            pex.dp);                          \
         ADR_LAUNCH_CHECK();                                                                                   \
         const int64_t hl = nb << RB;                                                                          \
-        scan_u32_exclusive<8><<<ceil_div(hl, 256 * 8), 256, 0, st>>>(hist, hl, status, counter);              \
+        scan_u32_exclusive<8><<<ceil_div(hl, 256 * 8), 256, 0, st>>>(hist, hl, status, counter, pex.dp);      \
         ADR_LAUNCH_CHECK();                                                                                   \
         const size_t dsm = downsweep_smem<K, V, RB>();                                                        \
         const int mode = last ? extra.mode : 0;                                                               \
+        (void)mode;                                                                                           \
         if (mode == 1) {                                                                                      \
             ADR_CUDA_TRY(cudaFuncSetAttribute(radix_downsweep<K, V, RB, 1>,                                   \
                                               cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dsm));        \
             radix_downsweep<K, V, RB, 1><<<nb, kSortBlock, dsm, st>>>(src_k, src_v, dst_k, dst_v, d_n, n_max,  \
-                                                                      bit, hist, extra);                      \
+                                                                      bit, hist, pex);                        \
         } else if (mode == 3) {                                                                               \
             ADR_CUDA_TRY(cudaFuncSetAttribute(radix_downsweep<K, V, RB, 3>,                                   \
                                               cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dsm));        \
             radix_downsweep<K, V, RB, 3><<<nb, kSortBlock, dsm, st>>>(src_k, src_v, dst_k, dst_v, d_n, n_max,  \
-                                                                      bit, hist, extra);                      \
+                                                                      bit, hist, pex);                        \
         } else if (mode == 2) {                                                                               \
             ADR_CUDA_TRY(cudaFuncSetAttribute(radix_downsweep<K, V, RB, 2>,                                   \
                                               cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dsm));        \
             radix_downsweep<K, V, RB, 2><<<nb, kSortBlock, dsm, st>>>(src_k, src_v, dst_k, dst_v, d_n, n_max,  \
-                                                                      bit, hist, extra);                      \
+                                                                      bit, hist, pex);                        \
         } else {                                                                                              \
             ADR_CUDA_TRY(cudaFuncSetAttribute(radix_downsweep<K, V, RB, 0>,                                   \
                                               cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dsm));        \
             radix_downsweep<K, V, RB, 0><<<nb, kSortBlock, dsm, st>>>(src_k, src_v, dst_k, dst_v, d_n, n_max,  \
-                                                                      bit, hist, extra);                      \
+                                                                      bit, hist, pex);                        \
         }                                                                                                     \
         ADR_LAUNCH_CHECK();                                                                                   \
     } while (0)

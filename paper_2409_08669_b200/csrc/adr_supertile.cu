@@ -768,6 +768,12 @@ int32_t frame_binning_supertile(const FrameBinning& fb, cudaStream_t st) {
     dx.mode = 3;
     dx.gsrc = fb.gpack;
     dx.rinfo = rinfo;
+    if (fb.kminmax && fb.plan_mm) {   // key-range plan, reduced by extra blocks of pass 0's upsweep
+        dx.dp.plan = fb.plan_mm;
+        dx.dp.plan_out = fb.plan_mm;
+        dx.dp.kminmax = fb.kminmax;
+        dx.dp.nkb = ceil_div(n, 128);
+    }
     int32_t rc = radix_sort<uint32_t, uint32_t>(fb.dkey, nullptr, skey, sval, nullptr, n, 32, rs1,
                                                 radix_scratch_bytes<uint32_t, uint32_t>(n), st, dx);
     if (rc) return rc;
