@@ -571,7 +571,7 @@ __global__ void __launch_bounds__(256) k_st_place(StItems items, StGeom g, StCtl
                                                   uint64_t* __restrict__ keys_out) {
     __shared__ uint2 stage[kStageCap];
     __shared__ uint8_t stile[kStageCap];
-    __shared__ uint32_t scnt[8][64];
+    __shared__ uint2 scnt[64];          // per tile: the 8 warps' counts, one byte each
     __shared__ uint2 sitem[8][32];
     __shared__ uint2 gtile[64];        // (global position - local slot of the run, tile id)
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -606,24 +606,30 @@ __global__ void __launch_bounds__(256) k_st_place(StItems items, StGeom g, StCtl
         const uint64_t mk = lr ? lrect_mask(lr) : 0ull;
         const uint32_t clo = warp_transpose32((uint32_t)mk, lane);
         const uint32_t chi = warp_transpose32((uint32_t)(mk >> 32), lane);
-        scnt[warp][lane] = __popc(clo);
-        scnt[warp][lane + 32] = __popc(chi);
+        reinterpret_cast<uint8_t*>(&scnt[lane])[warp] = (uint8_t)__popc(clo);
+        reinterpret_cast<uint8_t*>(&scnt[lane + 32])[warp] = (uint8_t)__popc(chi);
         __syncthreads();
-        // B: tile-major slots.  Lane owns tiles lane and lane + 32.
-        uint32_t wpre_lo = 0, wpre_hi = 0, tot_lo = 0, tot_hi = 0;
-#pragma unroll
-        for (int w = 0; w < 8; ++w) {
-            const uint32_t a = scnt[w][lane], b = scnt[w][lane + 32];
-            wpre_lo += w < warp ? a : 0u;
-            wpre_hi += w < warp ? b : 0u;
-            tot_lo += a;
-            tot_hi += b;
+        // B: tile-major slots.  Lane owns tiles lane and lane + 32; per tile the
+        // 8 warp counts (<= 32 each) are bytes, prefix-summed in-register
+        // (x * 0x01010101: byte k = c0 + ... + ck, no carries below 256)
+        uint32_t wpre_lo, wpre_hi, tot_lo, tot_hi;
+        {
+            const uint2 a = scnt[lane], b = scnt[lane + 32];
+            const uint32_t pa0 = a.x * 0x01010101u, pa1 = a.y * 0x01010101u;
+            const uint32_t pb0 = b.x * 0x01010101u, pb1 = b.y * 0x01010101u;
+            const uint32_t ta0 = pa0 >> 24, tb0 = pb0 >> 24;
+            tot_lo = ta0 + (pa1 >> 24);
+            tot_hi = tb0 + (pb1 >> 24);
+            // exclusive prefix of warp `warp` (warp-uniform shifts)
+            wpre_lo = warp == 0 ? 0u : (warp <= 4 ? (pa0 >> (8 * (warp - 1))) & 0xffu : ta0 + ((pa1 >> (8 * (warp - 5))) & 0xffu));
+            wpre_hi = warp == 0 ? 0u : (warp <= 4 ? (pb0 >> (8 * (warp - 1))) & 0xffu : tb0 + ((pb1 >> (8 * (warp - 5))) & 0xffu));
         }
-        const uint32_t inc_lo = warp_inclusive_sum(tot_lo);
-        const uint32_t sum_lo = __shfl_sync(kFull, inc_lo, 31);
-        const uint32_t inc_hi = warp_inclusive_sum(tot_hi);
-        const uint32_t ls_lo = inc_lo - tot_lo, ls_hi = sum_lo + inc_hi - tot_hi;   // local run starts
-        const uint32_t ctotal = sum_lo + __shfl_sync(kFull, inc_hi, 31);
+        // both tile halves in one scan (each half sums to < 2^16)
+        const uint32_t inc = warp_inclusive_sum(tot_lo | (tot_hi << 16));
+        const uint32_t sums = __shfl_sync(kFull, inc, 31);
+        const uint32_t sum_lo = sums & 0xffffu;
+        const uint32_t ls_lo = (inc & 0xffffu) - tot_lo, ls_hi = sum_lo + (inc >> 16) - tot_hi;   // local run starts
+        const uint32_t ctotal = sum_lo + (sums >> 16);
         if (warp == 0) {
             int sx, sy;
             st_xy(g, s, &sx, &sy);
