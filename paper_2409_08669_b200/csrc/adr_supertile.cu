@@ -188,15 +188,15 @@ __global__ void __launch_bounds__(1024) k_st_scan1(uint32_t* __restrict__ H1, co
     for (int64_t b0 = 0; b0 < n1; b0 += 1024 * K) {
         const int64_t a = b0 + (int64_t)threadIdx.x * K;
         uint32_t v[K], sum = 0;
-        if (a < n1) {
+        if (a + K <= n1) {
             const uint4 p = *reinterpret_cast<const uint4*>(col + a), q = *reinterpret_cast<const uint4*>(col + a + 4);
             v[0] = p.x; v[1] = p.y; v[2] = p.z; v[3] = p.w; v[4] = q.x; v[5] = q.y; v[6] = q.z; v[7] = q.w;
+        } else {
+#pragma unroll
+            for (int k = 0; k < K; ++k) v[k] = a + k < n1 ? col[a + k] : 0u;
         }
 #pragma unroll
-        for (int k = 0; k < K; ++k) {
-            v[k] = a + k < n1 ? v[k] : 0u;
-            sum += v[k];
-        }
+        for (int k = 0; k < K; ++k) sum += v[k];
         uint32_t tot;
         uint32_t run = carry + block_exclusive_sum<uint32_t, 1024>(sum, sred, &tot);
         uint32_t o[K];
