@@ -49,7 +49,7 @@ constexpr int kL1Ranks = 256;         // ranks per L1 warp chunk
 constexpr int kL1Block = 8 * kL1Ranks; // ranks per L1 block (h1b column entry, scatter block)
 constexpr int kL1Cap = 4096;          // items staged per L1 scatter window
 constexpr int kChunk = 256;           // items per L2 chunk (= one 256-thread block)
-constexpr int kStageCap = 4096;       // pairs staged per placement window
+constexpr int kStageCap = 3072;       // pairs staged per placement window
 
 struct StGeom {
     int32_t tx, ty;      // tile grid
@@ -565,7 +565,7 @@ __global__ void __launch_bounds__(1024) k_st_scan2(uint32_t* __restrict__ U, StG
 //      (the warp's items on that tile, in rank order) and stage each item's
 //      {index, depth bits} at consecutive slots of the tile's run;
 //   D  (barrier) thread per slot: coalesced per-tile runs out; (barrier).
-__global__ void __launch_bounds__(256) k_st_place(StItems items, StGeom g, StCtl c, int64_t items_cap,
+__global__ void __launch_bounds__(256, 6) k_st_place(StItems items, StGeom g, StCtl c, int64_t items_cap,
                                                   const uint32_t* __restrict__ C2, const uint32_t* __restrict__ U,
                                                   const int64_t* __restrict__ d_pc, uint32_t* __restrict__ gidx_out,
                                                   uint64_t* __restrict__ keys_out) {
