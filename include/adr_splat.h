@@ -27,7 +27,7 @@
 extern "C" {
 #endif
 
-#define ADR_ABI_VERSION 1
+#define ADR_ABI_VERSION 2
 
 typedef enum {
     ADR_OK = 0,
@@ -233,9 +233,19 @@ typedef struct {
     int64_t pair_capacity;
     /* optional per-stage CUDA events (7 cudaEvent_t as void*), may be NULL */
     void* const* events;
+    /* nonzero: the Projection's mean2d, conic, opacity and color are written
+     * only into the render record — row i is 12 float32 at byte offset
+     * adr_frame_record_offset(...) + 48 i of d_scratch: mean2d = [0:2],
+     * conic = [2:5], opacity = [5], color = [6:9] (rows of invalid Gaussians
+     * zero) — and proj.d_mean2d / d_conic / d_opacity / d_color are not
+     * touched (the caller views the record instead: 36 bytes per Gaussian
+     * fewer to write).  0: every Projection array is written. */
+    int32_t projection_in_record;
 } adr_frame_buffers;
 
 size_t adr_frame_scratch_bytes(int64_t n, int32_t width, int32_t height, int64_t pair_capacity);
+/* Byte offset of the render record array inside the frame scratch. */
+size_t adr_frame_record_offset(int64_t n, int32_t width, int32_t height, int64_t pair_capacity);
 int32_t adr_render_frame(const adr_scene* scene, const adr_camera* cam, int32_t mode,
                          double alpha_low, double dilation, double term_threshold,
                          const adr_frame_buffers* buf, void* stream);

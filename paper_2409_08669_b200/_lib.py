@@ -32,7 +32,7 @@ EXPORTED = (
     "adr_touched_counts", "adr_inclusive_sum_scratch_bytes", "adr_inclusive_sum",
     "adr_duplicate_with_keys", "adr_sort_pairs_scratch_bytes", "adr_sort_pairs",
     "adr_identify_tile_ranges", "adr_render", "adr_exp_np_f32", "adr_selftest_exp", "adr_render_selfcheck",
-    "adr_frame_scratch_bytes", "adr_render_frame", "adr_image_loss_scratch_bytes", "adr_image_losses",
+    "adr_frame_scratch_bytes", "adr_frame_record_offset", "adr_render_frame", "adr_image_loss_scratch_bytes", "adr_image_losses",
     "adr_render_reference_scratch_bytes", "adr_render_reference",
 )
 
@@ -71,7 +71,7 @@ class FrameBuffers_t(ctypes.Structure):
                 ("d_stats", ctypes.c_void_p), ("d_hist", ctypes.c_void_p),
                 ("hist_bins", ctypes.c_int32), ("d_scratch", ctypes.c_void_p),
                 ("scratch_bytes", ctypes.c_size_t), ("pair_capacity", ctypes.c_int64),
-                ("events", ctypes.c_void_p)]
+                ("events", ctypes.c_void_p), ("projection_in_record", ctypes.c_int32)]
 
 
 def build(verbose: bool = False) -> Path:
@@ -116,6 +116,7 @@ def lib() -> ctypes.CDLL:
             "adr_selftest_exp": (i32, [vp, vp]),
             "adr_render_selfcheck": (i32, [i32, vp]),
             "adr_frame_scratch_bytes": (sz, [i64, i32, i32, i64]),
+            "adr_frame_record_offset": (sz, [i64, i32, i32, i64]),
             "adr_render_frame": (i32, [P(Scene_t), P(Camera_t), i32, dbl, dbl, dbl,
                                        P(FrameBuffers_t), vp]),
             "adr_image_loss_scratch_bytes": (sz, [i32, i32]),
@@ -127,7 +128,7 @@ def lib() -> ctypes.CDLL:
             fn = getattr(L, name)
             fn.restype = res
             fn.argtypes = args
-        if L.adr_abi_version() != 1:
+        if L.adr_abi_version() != 2:
             raise RuntimeError("libadrsplat ABI mismatch")
         _lib = L
     return _lib

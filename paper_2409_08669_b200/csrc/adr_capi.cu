@@ -32,6 +32,7 @@ struct FrameLayout {
     uint32_t* dkey;
     uint32_t* order;
     Record* rec;
+    size_t rec_offset;   // byte offset of rec inside the scratch
     uint2* gpack;
     uint32_t* kminmax;
     uint32_t* plan_mm;
@@ -46,6 +47,7 @@ size_t frame_bytes(int64_t n, int32_t tx, int32_t ty, int64_t cap, FrameLayout* 
     FrameLayout l;
     l.dkey = c.take<uint32_t>(n);
     l.order = c.take<uint32_t>(n);
+    l.rec_offset = c.used;
     l.rec = c.take<Record>(n);
     l.gpack = c.take<uint2>(n);
     l.kminmax = c.take<uint32_t>(2 * ceil_div(n > 0 ? n : 1, 128));
@@ -130,6 +132,12 @@ int32_t adr_render(const adr_projection* proj, int64_t n, const int64_t* d_gidx,
                               (float)term_threshold, d_pixels, d_counts, d_stats, d_hist, hist_bins, st);
 }
 
+size_t adr_frame_record_offset(int64_t n, int32_t width, int32_t height, int64_t pair_capacity) {
+    FrameLayout L;
+    frame_bytes(n, tiles_of(width), tiles_of(height), pair_capacity, &L, nullptr, 0);
+    return L.rec_offset;
+}
+
 size_t adr_frame_scratch_bytes(int64_t n, int32_t width, int32_t height, int64_t pair_capacity) {
     return frame_bytes(n, tiles_of(width), tiles_of(height), pair_capacity, nullptr, nullptr, 0) + 1024;
 }
@@ -163,6 +171,7 @@ int32_t adr_render_frame(const adr_scene* scene, const adr_camera* cam, int32_t 
     fp.tiles_x = tx;
     fp.tiles_y = ty;
     fp.kminmax = supertile_path(n_tiles, tx, ty) ? L.kminmax : nullptr;
+    fp.rec_only = buf->projection_in_record != 0;
     fp.plan_mm = fp.kminmax ? L.plan_mm : nullptr;
     int32_t rc = launch_preprocess(*scene, *cam, mode, alpha_low, dilation, buf->proj, &fp, st);
     if (rc) return rc;

@@ -81,6 +81,7 @@ struct FusedPre {
     uint32_t* kminmax = nullptr;              // per block: min and max depth key of the selected rows
                                               // ([2 b] = min, [2 b + 1] = max; none: all-ones, 0)
     uint32_t* plan_mm = nullptr;              // the depth plan's (min, max), reset to (all-ones, 0) here
+    bool rec_only = false;                    // mean2d / conic / opacity / color only in the record
     int32_t tiles_x = 0, tiles_y = 0;
 };
 

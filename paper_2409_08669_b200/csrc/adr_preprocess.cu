@@ -239,18 +239,20 @@ k_preprocess(const T* __restrict__ centers, const T* __restrict__ scales,
             const float op = __double2float_rn(sigma);
             const float c0f = __double2float_rn(col[0]), c1f = __double2float_rn(col[1]),
                         c2f = __double2float_rn(col[2]);
-            reinterpret_cast<float2*>(out.d_mean2d)[i] = m2;
+            if (!(FUSED && fused.rec_only)) {   // else these live in the render record only
+                reinterpret_cast<float2*>(out.d_mean2d)[i] = m2;
+                out.d_conic[3 * i] = ca;
+                out.d_conic[3 * i + 1] = cb;
+                out.d_conic[3 * i + 2] = cc;
+                out.d_color[3 * i] = c0f;
+                out.d_color[3 * i + 1] = c1f;
+                out.d_color[3 * i + 2] = c2f;
+                out.d_opacity[i] = op;
+            }
             out.d_cov2d[3 * i] = __double2float_rn(sxx);
             out.d_cov2d[3 * i + 1] = __double2float_rn(syy);
             out.d_cov2d[3 * i + 2] = __double2float_rn(sxy);
-            out.d_conic[3 * i] = ca;
-            out.d_conic[3 * i + 1] = cb;
-            out.d_conic[3 * i + 2] = cc;
             out.d_depth[i] = dz;
-            out.d_color[3 * i] = c0f;
-            out.d_color[3 * i + 1] = c1f;
-            out.d_color[3 * i + 2] = c2f;
-            out.d_opacity[i] = op;
             out.d_lambda_max[i] = __double2float_rn(lam_max);
             const int32_t ix = np_i32(ex), iy = np_i32(ey);
             out.d_ext_x[i] = ix;
@@ -271,12 +273,19 @@ k_preprocess(const T* __restrict__ centers, const T* __restrict__ scales,
                                             (uint32_t)r.y0 | ((uint32_t)r.y1 << 16));
             }
         } else {
-            reinterpret_cast<float2*>(out.d_mean2d)[i] = make_float2(0.f, 0.f);
+            if (FUSED && fused.rec_only) {
+                const float4 z = make_float4(0.f, 0.f, 0.f, 0.f);
+                Record R;
+                R.a = R.b = R.c = z;
+                fused.rec[i] = R;
+            } else {
+                reinterpret_cast<float2*>(out.d_mean2d)[i] = make_float2(0.f, 0.f);
+                out.d_conic[3 * i] = out.d_conic[3 * i + 1] = out.d_conic[3 * i + 2] = 0.f;
+                out.d_color[3 * i] = out.d_color[3 * i + 1] = out.d_color[3 * i + 2] = 0.f;
+                out.d_opacity[i] = 0.f;
+            }
             out.d_cov2d[3 * i] = out.d_cov2d[3 * i + 1] = out.d_cov2d[3 * i + 2] = 0.f;
-            out.d_conic[3 * i] = out.d_conic[3 * i + 1] = out.d_conic[3 * i + 2] = 0.f;
             out.d_depth[i] = 0.f;
-            out.d_color[3 * i] = out.d_color[3 * i + 1] = out.d_color[3 * i + 2] = 0.f;
-            out.d_opacity[i] = 0.f;
             out.d_lambda_max[i] = 0.f;
             out.d_ext_x[i] = 0;
             out.d_ext_y[i] = 0;

@@ -174,6 +174,13 @@ class Rasterizer:
         self.scratch = torch.empty(nbytes, dtype=torch.uint8, device=dev)
         self.cap = cap
         self.generation += 1
+        # the frame writes mean2d / conic / opacity / color only into its
+        # 48-byte render record (adr_frame_buffers.projection_in_record): the
+        # Projection's four fields are strided views of that record
+        off = _lib.lib().adr_frame_record_offset(self.n, self.width, self.height, cap)
+        rec = self.scratch[off: off + 48 * self.n].view(torch.float32).view(self.n, 12)
+        self.proj.mean2d, self.proj.conic = rec[:, 0:2], rec[:, 2:5]
+        self.proj.opacity, self.proj.color = rec[:, 5], rec[:, 6:9]
 
     def fit_capacity(self, pairs: int, slack: float = 1.02) -> None:
         """Size the pair buffers to `pairs` (+slack): grids of the pair-parallel
@@ -185,7 +192,7 @@ class Rasterizer:
 
     def _buffers(self, timed: bool) -> _lib.FrameBuffers_t:
         b = _lib.FrameBuffers_t()
-        b.proj = self.proj.struct()
+        b.proj = self.proj.struct(contiguous=False)
         b.d_pixels, b.d_load = _lib.ptr(self.pixels), _lib.ptr(self.load)
         b.d_keys = _lib.ptr(self.keys) if self.export_pairs else None
         b.d_gidx = _lib.ptr(self.gidx)
@@ -194,6 +201,7 @@ class Rasterizer:
         b.d_scratch, b.scratch_bytes = _lib.ptr(self.scratch), self.scratch.numel()
         b.pair_capacity = self.cap
         b.events = ctypes.cast(self._ev_handles, ctypes.c_void_p) if (timed and self._ev_handles) else None
+        b.projection_in_record = 1
         return b
 
     # -- frames -------------------------------------------------------------

@@ -61,18 +61,33 @@ class Projection:
     def culled_count(self) -> int:
         return int((~self.valid).sum().item())
 
-    def struct(self) -> _lib.Projection_t:
+    def struct(self, contiguous: bool = True) -> _lib.Projection_t:
+        """C view of the arrays.  The library reads and writes them as
+        contiguous SoA, so strided fields (a fused frame's views into its
+        render record) are passed as contiguous copies, kept alive on the
+        object; ``contiguous=False`` passes the raw pointers (the frame call,
+        which does not touch those fields)."""
         p = _lib.Projection_t()
+        keep = []
         for name in _ARRAY_FIELDS:
-            setattr(p, "d_" + name, _lib.ptr(getattr(self, name)))
+            t = getattr(self, name)
+            if contiguous and not t.is_contiguous():
+                t = t.contiguous()
+                keep.append(t)
+            setattr(p, "d_" + name, _lib.ptr(t))
+        self._struct_copies = keep
         return p
 
     def to_numpy(self) -> dict:
         return {name: getattr(self, name).cpu().numpy() for name in _ARRAY_FIELDS}
 
     def clone(self) -> "Projection":
+        """Contiguous copies of every array (also of record-backed views)."""
+        import torch
+
         return Projection(mode=self.mode, alpha_low=self.alpha_low,
-                          **{name: getattr(self, name).clone() for name in _ARRAY_FIELDS})
+                          **{name: getattr(self, name).clone(memory_format=torch.contiguous_format)
+                             for name in _ARRAY_FIELDS})
 
     @classmethod
     def empty(cls, n: int, mode, alpha_low, device) -> "Projection":
