@@ -48,6 +48,7 @@ constexpr int kStSide = 8;            // supertile side in tiles
 constexpr int kL1Ranks = 256;         // ranks per L1 warp chunk
 constexpr int kL1Block = 8 * kL1Ranks; // ranks per L1 block (h1b column entry, scatter block)
 constexpr int kL1Cap = 4096;          // items staged per L1 scatter window
+constexpr int kXList = 64;            // per-warp expanded-item list of the L1 scatter (one round segment)
 constexpr int kChunk = 256;           // items per L2 chunk (= one 256-thread block)
 constexpr int kStageCap = 3072;       // pairs staged per placement window
 
@@ -114,16 +115,6 @@ __device__ __forceinline__ uint64_t lrect_mask(uint32_t lr) {
     const uint64_t hi = y1 >= 8 ? ~0ull : ((1ull << (8 * y1)) - 1ull);
     const uint64_t rows = 0x0101010101010101ull & hi & ~((1ull << (8 * y0)) - 1ull);
     return (uint64_t)row * rows;
-}
-
-// Owner lane of stream position base + lane: lanes own ascending, distinct
-// start offsets o (lanes with has == false own nothing); returns the last
-// owning lane whose start is <= base + lane.
-__device__ __forceinline__ int stream_owner(bool has, uint32_t o, uint32_t base, int lane) {
-    const uint32_t before = __popc(__ballot_sync(kFull, has && o < base));
-    const uint32_t d = o - base;
-    const uint32_t starts = __reduce_or_sync(kFull, (has && o >= base && d < 32u) ? (1u << d) : 0u);
-    return (int)(before + __popc(starts & ((2u << lane) - 1u))) - 1;
 }
 
 // ---------------------------------------------------------------- L1
@@ -252,19 +243,20 @@ __global__ void __launch_bounds__(1024) k_st_scan1(uint32_t* __restrict__ H1, co
 
 // Place the items, stably in rank order within each supertile bucket.  Block
 // = 2048 ranks, warp = 256 ranks (held in registers: a per-warp supertile
-// histogram first, then the placement).  Per round of 32 ranks a warp's items form a
-// stream in (rank, supertile) order; lanes take consecutive stream positions
-// (balanced however many supertiles a rank touches), peers with the same
-// supertile come from match.any and the lowest peer bumps the warp's running
-// offset.  Items are staged in shared memory in bucket order (the block's
+// histogram first, then the placement).  Per round of 32 ranks a warp's items
+// form a stream in (rank, supertile) order; each lane writes its own items
+// into a per-warp shared list at their stream positions, then lanes take 32
+// consecutive entries, peers with the same supertile come from match.any and
+// the lowest peer bumps the warp's running offset.  Items are staged in shared memory in bucket order (the block's
 // items of one supertile are contiguous in the output) and flushed as
 // coalesced runs.
 __global__ void __launch_bounds__(256, 4) k_st_scatter1(const uint4* __restrict__ rinfo, const int64_t* __restrict__ d_m,
                                                      StGeom g, const uint32_t* __restrict__ H1, StCtl c,
                                                      StItems items, int64_t items_cap) {
     extern __shared__ __align__(16) unsigned char sc_raw[];
-    uint2* sgd = reinterpret_cast<uint2*>(sc_raw);                               // [kL1Cap]
-    uint16_t* slr = reinterpret_cast<uint16_t*>(sc_raw + 8 * kL1Cap);             // [kL1Cap]
+    uint4* xlist = reinterpret_cast<uint4*>(sc_raw);                             // [8][kXList] expanded items
+    uint2* sgd = reinterpret_cast<uint2*>(xlist + 8 * kXList);                   // [kL1Cap]
+    uint16_t* slr = reinterpret_cast<uint16_t*>(sgd + kL1Cap);                   // [kL1Cap]
     uint16_t* sdig = slr + kL1Cap;                                               // [kL1Cap]
     uint32_t* wbase = reinterpret_cast<uint32_t*>(sdig + kL1Cap);                // [8][S] warp slot bases
     uint32_t* woff = wbase + 8 * g.S;                                            // [8][S] running
@@ -277,19 +269,19 @@ __global__ void __launch_bounds__(256, 4) k_st_scatter1(const uint4* __restrict_
     const int64_t b = blockIdx.x;
     const int64_t r0 = b * kL1Block + warp * kL1Ranks;
     const int64_t r1 = r0 + kL1Ranks < m ? r0 + kL1Ranks : m;
-    // this warp's ranks, and its items per supertile (shared-memory histogram)
-    uint4 vb[kR];
+    // this warp's ranks' rectangles, and its items per supertile (shared-memory histogram)
+    uint2 vb[kR];
 #pragma unroll
     for (int k = 0; k < kR; ++k) {
         const int64_t r = r0 + k * 32 + lane;
-        vb[k] = r < r1 ? rinfo[r] : make_uint4(0u, 0u, 0u, 0u);
+        vb[k] = r < r1 ? __ldg(reinterpret_cast<const uint2*>(rinfo + r) + 1) : make_uint2(0u, 0u);
     }
     uint32_t* wh = wbase + warp * g.S;
     for (int s = lane; s < g.S; s += 32) wh[s] = 0;
     __syncwarp();
 #pragma unroll
     for (int k = 0; k < kR; ++k) {
-        const uint32_t x0 = vb[k].z & 0xffffu, x1 = vb[k].z >> 16, y0 = vb[k].w & 0xffffu, y1 = vb[k].w >> 16;
+        const uint32_t x0 = vb[k].x & 0xffffu, x1 = vb[k].x >> 16, y0 = vb[k].y & 0xffffu, y1 = vb[k].y >> 16;
         if (x1 > x0)
             for (uint32_t sy = y0 >> 3; sy <= (y1 - 1) >> 3; ++sy)
                 for (uint32_t sx = x0 >> 3; sx <= (x1 - 1) >> 3; ++sx) atomicAdd(&wh[sy * g.sxn + sx], 1u);
@@ -357,51 +349,62 @@ __global__ void __launch_bounds__(256, 4) k_st_scatter1(const uint4* __restrict_
         for (int s = lane; s < g.S; s += 32) off[s] = lst[s] + wbase[warp * g.S + s];
         __syncwarp();
         if (r0 < r1) {
-#pragma unroll
+            uint4* xl = xlist + warp * kXList;
+            uint4 vn = rinfo[r0 + lane < r1 ? r0 + lane : r0];
+#pragma unroll 1
             for (int k = 0; k < kR; ++k) {
-                const uint4 v = vb[k];
+                // the round's items in stream order (rank, then supertile): each
+                // lane expands its own rank's items into the warp's list ...
+                const bool in = r0 + k * 32 + lane < r1;
+                const uint4 v = in ? vn : make_uint4(0u, 0u, 0u, 0u);
+                if (k + 1 < kR) {   // next round's rank record (L2-hot: read by the histogram above)
+                    const int64_t rn = r0 + (k + 1) * 32 + lane;
+                    vn = rinfo[rn < r1 ? rn : r0];
+                }
                 const uint32_t x0 = v.z & 0xffffu, x1 = v.z >> 16, y0 = v.w & 0xffffu, y1 = v.w >> 16;
                 const bool has = x1 > x0;
-                const uint32_t sx0 = x0 >> 3, sy0 = y0 >> 3;
-                const uint32_t nsx = has ? ((x1 - 1) >> 3) - sx0 + 1 : 0u;
-                const uint32_t cnt = has ? nsx * (((y1 - 1) >> 3) - sy0 + 1) : 0u;
+                const uint32_t sx0 = x0 >> 3, sy0 = y0 >> 3, sx1 = has ? (x1 - 1) >> 3 : 0u, sy1 = has ? (y1 - 1) >> 3 : 0u;
+                const uint32_t cnt = has ? (sx1 - sx0 + 1) * (sy1 - sy0 + 1) : 0u;
                 const uint32_t incl = warp_inclusive_sum(cnt);
                 const uint32_t o = incl - cnt;
                 const uint32_t total = __shfl_sync(kFull, incl, 31);
-                for (uint32_t base = 0; base < total; base += 32) {
-                    const int L = stream_owner(has, o, base, lane);
-                    const uint32_t oL = __shfl_sync(kFull, o, L);
-                    const uint32_t nsxL = __shfl_sync(kFull, nsx, L);
-                    const uint32_t zL = __shfl_sync(kFull, v.z, L), wL = __shfl_sync(kFull, v.w, L);
-                    const uint32_t gL = __shfl_sync(kFull, v.x, L), dL = __shfl_sync(kFull, v.y, L);
-                    const uint32_t q = base + lane;
-                    const bool live = q < total;
-                    uint32_t j = q - oL, jy = 0;
-                    if (live)
-                        while (j >= nsxL) {   // nsx is 1 or 2 for nearly every rank
-                            j -= nsxL;
-                            ++jy;
-                        }
-                    const uint32_t sx = ((zL & 0xffffu) >> 3) + j, sy = ((wL & 0xffffu) >> 3) + jy;
-                    const uint32_t s = live ? sy * g.sxn + sx : 0xffffffffu;
-                    const uint32_t peers = __match_any_sync(kFull, s);
-                    const uint32_t ob = live ? off[s] : 0u;
-                    __syncwarp();
-                    if (live) {
-                        if ((peers & lt) == 0) off[s] = ob + __popc(peers);
-                        const uint32_t slot = ob + __popc(peers & lt) - win;
-                        if (slot < (uint32_t)kL1Cap) {
-                            const uint32_t X0 = zL & 0xffffu, X1 = zL >> 16, Y0 = wL & 0xffffu, Y1 = wL >> 16;
-                            const uint32_t lx0 = (X0 > sx * 8 ? X0 : sx * 8) - sx * 8;
-                            const uint32_t lx1 = (X1 < sx * 8 + 8 ? X1 : sx * 8 + 8) - sx * 8;
-                            const uint32_t ly0 = (Y0 > sy * 8 ? Y0 : sy * 8) - sy * 8;
-                            const uint32_t ly1 = (Y1 < sy * 8 + 8 ? Y1 : sy * 8 + 8) - sy * 8;
-                            sgd[slot] = make_uint2(gL, dL);
-                            slr[slot] = (uint16_t)(lx0 | (lx1 << 4) | (ly0 << 8) | (ly1 << 12));
-                            sdig[slot] = (uint16_t)s;
+                for (uint32_t seg = 0; seg < total; seg += kXList) {
+                    if (has && o < seg + kXList && o + cnt > seg) {
+                        uint32_t q = o;
+                        for (uint32_t sy = sy0; sy <= sy1; ++sy) {
+                            const uint32_t ly0 = (y0 > sy * 8 ? y0 : sy * 8) - sy * 8;
+                            const uint32_t ly1 = (y1 < sy * 8 + 8 ? y1 : sy * 8 + 8) - sy * 8;
+                            for (uint32_t sx = sx0; sx <= sx1; ++sx, ++q) {
+                                if (q - seg >= (uint32_t)kXList) continue;
+                                const uint32_t lx0 = (x0 > sx * 8 ? x0 : sx * 8) - sx * 8;
+                                const uint32_t lx1 = (x1 < sx * 8 + 8 ? x1 : sx * 8 + 8) - sx * 8;
+                                xl[q - seg] = make_uint4(v.x, v.y, lx0 | (lx1 << 4) | (ly0 << 8) | (ly1 << 12),
+                                                         sy * g.sxn + sx);
+                            }
                         }
                     }
                     __syncwarp();
+                    // ... then 32 consecutive entries at a time are ranked among
+                    // equal supertiles (match.any; lane order = stream order) and
+                    // staged at the warp's running bucket offsets
+                    const uint32_t nseg = total - seg < (uint32_t)kXList ? total - seg : (uint32_t)kXList;
+                    for (uint32_t base = 0; base < nseg; base += 32) {
+                        const bool live = base + lane < nseg;
+                        const uint4 e = live ? xl[base + lane] : make_uint4(0u, 0u, 0u, 0xffffffffu);
+                        const uint32_t peers = __match_any_sync(kFull, e.w);
+                        const uint32_t ob = live ? off[e.w] : 0u;
+                        __syncwarp();
+                        if (live) {
+                            if ((peers & lt) == 0) off[e.w] = ob + __popc(peers);
+                            const uint32_t slot = ob + __popc(peers & lt) - win;
+                            if (slot < (uint32_t)kL1Cap) {
+                                sgd[slot] = make_uint2(e.x, e.y);
+                                slr[slot] = (uint16_t)e.z;
+                                sdig[slot] = (uint16_t)e.w;
+                            }
+                        }
+                        __syncwarp();
+                    }
                 }
             }
         }
@@ -791,7 +794,7 @@ int32_t frame_binning_supertile(const FrameBinning& fb, cudaStream_t st) {
     ADR_LAUNCH_CHECK();
     k_st_scan1<<<(unsigned)g.S, 1024, 0, st>>>(H1, ctr + 2, g, c, icap, ctr, fb.stats);
     ADR_LAUNCH_CHECK();
-    const size_t sm_sc = 12 * (size_t)kL1Cap + (18 * (size_t)g.S + 2) * sizeof(uint32_t);  // see k_st_scatter1
+    const size_t sm_sc = 16 * 8 * (size_t)kXList + 12 * (size_t)kL1Cap + (18 * (size_t)g.S + 2) * sizeof(uint32_t);  // see k_st_scatter1
     ADR_CUDA_TRY(cudaFuncSetAttribute(k_st_scatter1, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm_sc));
     k_st_scatter1<<<nb1, 256, sm_sc, st>>>(rinfo, ctr + 2, g, H1, c, items, icap);
     ADR_LAUNCH_CHECK();
