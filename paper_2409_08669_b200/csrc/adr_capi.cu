@@ -1,6 +1,7 @@
 // adr_capi.cu — extern "C" entry points of libadrsplat (include/adr_splat.h)
 // and the fused frame (sb/pipeline.py:85-124).
 #include <atomic>
+#include <cmath>
 #include <climits>
 #include <string>
 
@@ -172,6 +173,7 @@ int32_t adr_render_frame(const adr_scene* scene, const adr_camera* cam, int32_t 
     fp.tiles_y = ty;
     fp.kminmax = supertile_path(n_tiles, tx, ty) ? L.kminmax : nullptr;
     fp.rec_only = buf->projection_in_record != 0;
+    fp.ln_a32_a64 = std::log((double)(float)alpha_low / alpha_low);
     fp.plan_mm = fp.kminmax ? L.plan_mm : nullptr;
     int32_t rc = launch_preprocess(*scene, *cam, mode, alpha_low, dilation, buf->proj, &fp, st);
     if (rc) return rc;

@@ -35,8 +35,13 @@ struct __align__(16) Record {
 //              Slow splats get an infinite box (no culling).
 // A contribution is only skipped when the reference provably skips it, so
 // the image and load map stay bit-identical.
+// ln_a_over_op: ln(alpha_low32 / op) when the caller already has it (the
+// fused preprocess derives it from the extent's ln(sigma / alpha_low) plus a
+// per-frame constant, within ~1e-7 — inside the 1e-5 margin, which is
+// widened by 2e-7 on that path); >= 1e300: computed here.
 __device__ inline void cull_params(float a, float b, float c, float op, float alpha_low32, float c0, float c1,
-                                   float c2, float* tau, float* hx, float* hy) {
+                                   float c2, float* tau, float* hx, float* hy,
+                                   double ln_a_over_op = 1e300) {
     const float kInf = __int_as_float(0x7f800000);
     if (!(op > 0.0f)) {
         *tau = kInf;
@@ -55,7 +60,8 @@ __device__ inline void cull_params(float a, float b, float c, float op, float al
     const double M = (da > dc ? da : dc) + 0.5 * fabs(db);
     const double eta = 2.0 * 8.0 * 5.9604644775390625e-08 * M / lmin;
     if (!(eta < 0.25)) return;
-    const double t = log((double)alpha_low32 / (double)op) - 1e-5;
+    const double t = ln_a_over_op < 1e299 ? ln_a_over_op - 1.02e-5
+                                                  : log((double)alpha_low32 / (double)op) - 1e-5;
     float t32 = __double2float_rd(t);
     t32 = t32 > -87.0f ? t32 : -87.0f;
     *tau = t32;
@@ -82,6 +88,7 @@ struct FusedPre {
                                               // ([2 b] = min, [2 b + 1] = max; none: all-ones, 0)
     uint32_t* plan_mm = nullptr;              // the depth plan's (min, max), reset to (all-ones, 0) here
     bool rec_only = false;                    // mean2d / conic / opacity / color only in the record
+    double ln_a32_a64 = 0.0;                  // ln((double)(float)alpha_low / alpha_low), for cull_params
     int32_t tiles_x = 0, tiles_y = 0;
 };
 

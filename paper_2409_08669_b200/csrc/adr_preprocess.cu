@@ -193,12 +193,15 @@ k_preprocess(const T* __restrict__ centers, const T* __restrict__ scales,
         const double r_o_real = MUL(3.0, __dsqrt_rn(np_max(lam_max, 0.0)));
         const double sigma = (double)aop;
         double ex, ey;
+        double ln_a_over_op = 1e300;   // for cull_params (fused); 1e300: not known
+
         if (mode == ADR_MODE_BASELINE) {
             ex = ceil(r_o_real);
             ey = ex;
         } else {
             alive = alive && (sigma > alpha_low);
             const double log_ratio = log_fd(np_max(__ddiv_rn(sigma, alpha_low), 1e-300));
+            if (FUSED) ln_a_over_op = fused.ln_a32_a64 - log_ratio;   // = ln(a32 / sigma)
             if (mode == ADR_MODE_CIRCLE) {
                 const double v = __dsqrt_rn(MUL(MUL(2.0, lam_max), log_ratio));
                 ex = ceil(np_min(v, r_o_real));
@@ -264,7 +267,7 @@ k_preprocess(const T* __restrict__ centers, const T* __restrict__ scales,
                 dbits = __float_as_uint(dz);
                 Record R;
                 float tau, hx, hy;
-                cull_params(ca, cb, cc, op, (float)alpha_low, c0f, c1f, c2f, &tau, &hx, &hy);
+                cull_params(ca, cb, cc, op, (float)alpha_low, c0f, c1f, c2f, &tau, &hx, &hy, ln_a_over_op);
                 R.a = make_float4(m2.x, m2.y, ca, cb);
                 R.b = make_float4(cc, op, c0f, c1f);
                 R.c = make_float4(c2f, tau, hx, hy);
