@@ -165,6 +165,12 @@ int32_t adr_exp_np_f32(const float* d_x, float* d_y, int64_t n, void* stream);
  * checked, d_result[2] = smallest mismatching bit pattern (all-ones if none). */
 int32_t adr_selftest_exp(uint64_t* d_result, void* stream);
 
+/* Exhaustive pin of the render's exp against numpy's: *d_out = sum over the
+ * float32 bit patterns u in [lo, hi) of (bits(exp(u)) + 1) *
+ * (u * 0x9E3779B97F4A7C15 | 1) mod 2^64 — the checksum
+ * tests/golden/make_exp_exhaustive.py computes over np.exp(float32). */
+int32_t adr_exp_checksum(uint64_t lo, uint64_t hi, uint64_t* d_out, void* stream);
+
 /* Render self-check (test infrastructure, no reference counterpart).  With
  * enable != 0 the following frames launch the counting instantiation of the
  * tile blend, which iterates each warp's plain bounding box and counts every

@@ -57,7 +57,7 @@ static inline float scale_pow2(float v, int k) {
 }
 
 float orc_exp_np(float x) {
-    if (x != x) return x;
+    if (x != x) return f_from_bits(0x7fc00000u);   /* numpy returns the canonical quiet NaN for every NaN */
     if (x > 88.72283935546875f) return INFINITY;
     if (x < -103.97208404541015625f) return 0.0f;
     float q = x * 1.442695040888963407359924681001892137f;
@@ -531,4 +531,28 @@ void orc_render(int32_t width, int32_t height, int32_t tiles_x, int32_t tiles_y,
     }
     (void)tiles_y;
     (void)nthreads;
+}
+
+/* Exhaustive pin of orc_exp_np (test infrastructure): over every float32 bit
+ * pattern u in [lo, hi), H = sum of (y + 1) * (u * 0x9E3779B97F4A7C15 | 1)
+ * mod 2^64 with y = the output bits (order-independent; any changed output
+ * changes H).  tests/golden/make_exp_exhaustive.py computes the same sum over
+ * numpy's own np.exp(float32). */
+uint64_t orc_exp_checksum(uint64_t lo, uint64_t hi) {
+    uint64_t total = 0;
+#pragma omp parallel for reduction(+ : total) schedule(static)
+    for (int64_t c = (int64_t)(lo >> 20); c < (int64_t)((hi + 0xfffff) >> 20); ++c) {
+        uint64_t s = 0;
+        const uint64_t a = (uint64_t)c << 20, b = ((uint64_t)c + 1) << 20;
+        for (uint64_t u = a < lo ? lo : a; u < (b < hi ? b : hi); ++u) {
+            float x;
+            uint32_t ub = (uint32_t)u, yb;
+            memcpy(&x, &ub, 4);
+            const float y = orc_exp_np(x);
+            memcpy(&yb, &y, 4);
+            s += ((uint64_t)yb + 1u) * ((u * 0x9E3779B97F4A7C15ull) | 1u);
+        }
+        total += s;
+    }
+    return total;
 }

@@ -67,6 +67,8 @@ def lib():
         _lib = ctypes.CDLL(str(_LIB_PATH))
         _lib.orc_exp_np.restype = ctypes.c_float
         _lib.orc_exp_np.argtypes = [ctypes.c_float]
+        _lib.orc_exp_checksum.restype = ctypes.c_uint64
+        _lib.orc_exp_checksum.argtypes = [ctypes.c_uint64, ctypes.c_uint64]
         _lib.orc_log.restype = ctypes.c_double
         _lib.orc_log.argtypes = [ctypes.c_double]
         _lib.orc_inclusive_sum.restype = ctypes.c_int32

@@ -8,6 +8,7 @@
 //                       lane) equal exp_np on every float32 in [-87, 88].
 #include "adr_common.cuh"
 #include "adr_f32x2.cuh"
+#include "adr_scan.cuh"
 
 namespace adr {
 namespace {
@@ -38,6 +39,20 @@ __global__ void k_selftest_exp(unsigned long long* mismatches, unsigned int* fir
     atomicAdd(checked, seen);
 }
 
+// Exhaustive pin against numpy: H = sum over u in [lo, hi) of
+// (bits(exp_np(u)) + 1) * (u * 0x9E3779B97F4A7C15 | 1) mod 2^64, the same
+// checksum tests/golden/make_exp_exhaustive.py computes over np.exp.
+__global__ void k_exp_checksum(uint64_t lo, uint64_t hi, unsigned long long* out) {
+    uint64_t s = 0;
+    const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+    for (uint64_t u = lo + (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; u < hi; u += stride) {
+        const uint32_t y = __float_as_uint(exp_np(__uint_as_float((uint32_t)u)));
+        s += ((uint64_t)y + 1u) * ((u * 0x9E3779B97F4A7C15ull) | 1u);
+    }
+    s = warp_sum(s);
+    if ((threadIdx.x & 31) == 0) atomicAdd(out, (unsigned long long)s);
+}
+
 }  // namespace
 }  // namespace adr
 
@@ -49,6 +64,15 @@ int32_t adr_exp_np_f32(const float* d_x, float* d_y, int64_t n, void* stream) {
     if (n <= 0) return ADR_OK;
     const int64_t blocks = ceil_div(n, 256) < 4096 ? ceil_div(n, 256) : 4096;
     k_exp_np<<<blocks, 256, 0, as_stream(stream)>>>(d_x, d_y, n);
+    ADR_LAUNCH_CHECK();
+    return ADR_OK;
+}
+
+int32_t adr_exp_checksum(uint64_t lo, uint64_t hi, uint64_t* d_out, void* stream) {
+    cudaStream_t st = as_stream(stream);
+    ADR_CUDA_TRY(cudaMemsetAsync(d_out, 0, sizeof(uint64_t), st));
+    if (hi <= lo) return ADR_OK;
+    k_exp_checksum<<<148 * 8, 256, 0, st>>>(lo, hi, reinterpret_cast<unsigned long long*>(d_out));
     ADR_LAUNCH_CHECK();
     return ADR_OK;
 }

@@ -11,7 +11,7 @@ import hashlib
 import numpy as np
 import pytest
 
-from conftest import (GOLDEN_CASES, PROJ_FIELDS, SEMANTIC_CASES, bits_equal, config1_digests, gaussian,
+from conftest import (GOLDEN, GOLDEN_CASES, PROJ_FIELDS, SEMANTIC_CASES, bits_equal, config1_digests, gaussian,
                       golden_arrays, golden_camera, load_golden, make_camera, make_scene,
                       mixed_spec, nan_bits_equal)
 
@@ -242,6 +242,30 @@ def test_gpu_exp_matches_numpy_golden_vectors():
     nan = np.isnan(y.view(np.float32))
     assert np.array_equal(got[~nan], y[~nan])
     assert np.all(np.isnan(got.view(np.float32)[nan]))
+
+
+def test_exp_equals_numpy_on_every_float32():
+    """The render's exp_np equals numpy's float32 exp on ALL 2^32 inputs (and
+    on the fast path's [-87, 88]): its checksum over every bit pattern equals
+    the one numpy computed in the build container
+    (tests/golden/make_exp_exhaustive.py, sb/render.py:96)."""
+    import json
+
+    import torch
+
+    from paper_2409_08669_b200 import _lib
+
+    g = json.loads((GOLDEN / "exp_exhaustive.json").read_text())
+    out = torch.zeros(1, dtype=torch.int64, device="cuda")
+    st = _lib.stream_handle(torch.cuda.current_stream())
+    _lib.check(_lib.lib().adr_exp_checksum(0, 1 << 32, _lib.ptr(out), st))
+    assert int(out.item()) % (1 << 64) == g["all_2p32"]
+    lo87 = int(np.float32(-87.0).view(np.uint32))
+    hi88 = int(np.float32(88.0).view(np.uint32))
+    _lib.check(_lib.lib().adr_exp_checksum(0, hi88 + 1, _lib.ptr(out), st))
+    a = int(out.item()) % (1 << 64)
+    _lib.check(_lib.lib().adr_exp_checksum(0x80000000, lo87 + 1, _lib.ptr(out), st))
+    assert (a + int(out.item())) % (1 << 64) == g["range_m87_88"]
 
 
 def test_exp_fast_path_exhaustive():
