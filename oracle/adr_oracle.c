@@ -136,9 +136,12 @@ double orc_log(double x) {
 }
 
 /* numpy's NaN-propagating minimum/maximum (np.minimum / np.maximum). */
-static inline double np_min(double a, double b) { return (a != a || b != b) ? NAN : (a < b ? a : b); }
-static inline double np_max(double a, double b) { return (a != a || b != b) ? NAN : (a > b ? a : b); }
-static inline double np_clip(double v, double lo, double hi) { return np_min(np_max(v, lo), hi); }
+/* numpy's minimum / maximum (ties give the second operand, a NaN operand is
+ * returned) and clip (v unless strictly outside [lo, hi]; NaN stays), as the
+ * AVX-512 array loops behave, signed zeros included. */
+static inline double np_min(double a, double b) { return (a < b || a != a) ? a : b; }
+static inline double np_max(double a, double b) { return (a > b || a != a) ? a : b; }
+static inline double np_clip(double v, double lo, double hi) { return v < lo ? lo : (v > hi ? hi : v); }
 
 /* SH constants, projection.py:119-125. */
 static const double SH_C0 = 0.28209479177387814;

@@ -8,6 +8,10 @@
 //  * c_t = cov3d @ t (batched dgemv) → fma(cov2,t2, fma(cov0,t0, cov1*t1));
 //  * np.sum over 3 terms → (a+b)+c; outputs rounded fp64→fp32 (RN).
 #include "adr_kernels.cuh"
+
+#ifndef PRE_BLOCKS_PER_SM
+#define PRE_BLOCKS_PER_SM 0
+#endif
 #include "adr_scan.cuh"
 
 namespace adr {
@@ -56,6 +60,9 @@ __device__ __forceinline__ double sh_channel(const double* c, double x, double y
 }
 
 constexpr int kPreBlock = 128;
+// Fused frames may cap the preprocess grid at kPreBlocksPerSm blocks per SM
+// (grid-stride); measured no better than the full grid (notes.md, exp. 8).
+constexpr int kPreBlocksPerSm = PRE_BLOCKS_PER_SM;   // fused frames: resident blocks per SM (0: one per 128 Gaussians)
 
 // SH coefficients of the block's Gaussians are staged through shared memory:
 // one coalesced pass over the block's contiguous (128, K, 3) slab, stored with
@@ -94,16 +101,16 @@ __device__ __forceinline__ void stage_sh(const T* __restrict__ sh, int64_t first
 }
 
 template <typename T, int DEG, bool FUSED>
-__global__ void __launch_bounds__(kPreBlock)
-k_preprocess(const T* __restrict__ centers, const T* __restrict__ scales,
-             const T* __restrict__ rotations, const T* __restrict__ opacities,
-             const T* __restrict__ sh, int64_t n, adr_camera cam, int32_t mode,
-             double alpha_low, double dilation, adr_projection out, FusedPre fused) {
+__device__ __forceinline__ void preprocess_block(const T* __restrict__ centers, const T* __restrict__ scales,
+                                                 const T* __restrict__ rotations, const T* __restrict__ opacities,
+                                                 const T* __restrict__ sh, int64_t n, const adr_camera& cam,
+                                                 int32_t mode, double alpha_low, double dilation,
+                                                 const adr_projection& out, const FusedPre& fused, int64_t blk) {
     constexpr int K = (DEG + 1) * (DEG + 1);
     constexpr int S = K * 3 + 1;
     extern __shared__ __align__(16) unsigned char pre_smem[];
     T* stage = reinterpret_cast<T*>(pre_smem);
-    const int64_t first = (int64_t)blockIdx.x * kPreBlock;
+    const int64_t first = blk * kPreBlock;
     const int64_t i = first + threadIdx.x;
     // per-Gaussian attributes first, so their latency overlaps the SH staging
     T ac[3] = {T(0), T(0), T(0)}, as[3] = {T(0), T(0), T(0)}, aq[4] = {T(0), T(0), T(0), T(0)}, aop = T(0);
@@ -317,7 +324,7 @@ k_preprocess(const T* __restrict__ centers, const T* __restrict__ scales,
                 smm[2 * wid + 1] = kmx;
             }
             __syncthreads();
-            if (threadIdx.x == 0 && blockIdx.x == 0 && fused.plan_mm) {
+            if (threadIdx.x == 0 && blk == 0 && fused.plan_mm) {
                 fused.plan_mm[0] = 0xffffffffu;
                 fused.plan_mm[1] = 0u;
             }
@@ -327,8 +334,8 @@ k_preprocess(const T* __restrict__ centers, const T* __restrict__ scales,
                     a = smm[2 * w] < a ? smm[2 * w] : a;
                     b = smm[2 * w + 1] > b ? smm[2 * w + 1] : b;
                 }
-                fused.kminmax[2 * blockIdx.x] = a;
-                fused.kminmax[2 * blockIdx.x + 1] = b;
+                fused.kminmax[2 * blk] = a;
+                fused.kminmax[2 * blk + 1] = b;
             }
         }
         if (lane == 0) {
@@ -336,6 +343,23 @@ k_preprocess(const T* __restrict__ centers, const T* __restrict__ scales,
             if (sb) atomicAdd(reinterpret_cast<unsigned long long*>(fused.d_m), (unsigned long long)__popc(sb));
             if (nanb && fused.nan_colors) atomicAdd(fused.nan_colors, (unsigned long long)__popc(nanb));
         }
+    }
+}
+
+// Grid-stride over 128-Gaussian blocks.  Register budget pinned to 7 blocks
+// per SM (72 registers): with frames in flight, 64 registers (8 blocks) and
+// 80 (6 blocks) both measured 2-5% fewer frames/s (notes.md, experiment 8).
+template <typename T, int DEG, bool FUSED>
+__global__ void __launch_bounds__(kPreBlock, 7)
+k_preprocess(const T* __restrict__ centers, const T* __restrict__ scales,
+             const T* __restrict__ rotations, const T* __restrict__ opacities,
+             const T* __restrict__ sh, int64_t n, adr_camera cam, int32_t mode,
+             double alpha_low, double dilation, adr_projection out, FusedPre fused) {
+    const int64_t nblk = (n + kPreBlock - 1) / kPreBlock;
+    for (int64_t blk = blockIdx.x; blk < nblk; blk += gridDim.x) {
+        preprocess_block<T, DEG, FUSED>(centers, scales, rotations, opacities, sh, n, cam, mode, alpha_low,
+                                        dilation, out, fused, blk);
+        __syncthreads();   // the SH stage is rewritten by the next block
     }
 }
 
@@ -347,7 +371,17 @@ k_preprocess(const T* __restrict__ centers, const T* __restrict__ scales,
 template <typename T, bool FUSED>
 int32_t launch_typed(const adr_scene& s, const adr_camera& cam, int32_t mode, double alpha_low,
                      double dilation, const adr_projection& out, const FusedPre& f, cudaStream_t st) {
-    const int64_t grid = ceil_div(s.n, kPreBlock);
+    int64_t grid = ceil_div(s.n, kPreBlock);
+    if (FUSED && kPreBlocksPerSm > 0) {
+        static int sms = 0;
+        if (!sms) {
+            int dev = 0;
+            ADR_CUDA_TRY(cudaGetDevice(&dev));
+            ADR_CUDA_TRY(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+        }
+        const int64_t cap = (int64_t)sms * kPreBlocksPerSm;
+        grid = grid < cap ? grid : cap;
+    }
     const T* c = static_cast<const T*>(s.d_centers);
     const T* sc = static_cast<const T*>(s.d_scales);
     const T* r = static_cast<const T*>(s.d_rotations);
