@@ -271,13 +271,31 @@ def run_ours(args, cfg, rank, world, local):
     from paper_2409_08669_b200 import _lib
     from paper_2409_08669_b200.views import FrameGather, broadcast_scene, shard_views
 
-    torch.cuda.set_device(local)
-    dev = torch.device("cuda", local)
+    # one rank per GPU over NCCL; ADR_BENCH_BACKEND=gloo is a functional test of
+    # the multi-rank path on a one-GPU box (ranks share device 0; gloo moves
+    # the frames through host memory), never a measurement
+    backend = os.environ.get("ADR_BENCH_BACKEND", "nccl")
+    gpu = local if backend == "nccl" else local % max(torch.cuda.device_count(), 1)
+    torch.cuda.set_device(gpu)
+    dev = torch.device("cuda", gpu)
     dist = None
     if world > 1:
         import torch.distributed as dist
 
-        dist.init_process_group("nccl", device_id=dev)
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=dev)
+        else:
+            dist.init_process_group(backend)
+
+    def reduce_(t, op=None):
+        """all_reduce on the device over NCCL, through host memory over gloo."""
+        if backend == "nccl":
+            dist.all_reduce(t, op=op or dist.ReduceOp.SUM)
+            return t
+        h = t.cpu()
+        dist.all_reduce(h, op=op or dist.ReduceOp.SUM)
+        t.copy_(h)
+        return t
     L = _lib.lib()
     t_setup = time.perf_counter()
     # scene: built once on rank 0, broadcast to the others (SURVEY.md §8e)
@@ -360,7 +378,7 @@ def run_ours(args, cfg, rank, world, local):
         ms = e0.elapsed_time(e1)
         if dist:
             t = torch.tensor([ms], dtype=torch.float64, device=dev)
-            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            reduce_(t, op=dist.ReduceOp.MAX)
             ms = float(t.item())
         return ms
 
@@ -369,7 +387,7 @@ def run_ours(args, cfg, rank, world, local):
     torch.cuda.synchronize(dev)
     # render-only (no gather): the per-rank rendering rate
     ms_render = timed(args.steps, gather=False)
-    clocks = Clocks(local)
+    clocks = Clocks(gpu)
     clocks.start()
     time.sleep(0.3)
     ms = timed(args.steps, gather=True)   # the headline: render + gather to rank 0
@@ -384,7 +402,7 @@ def run_ours(args, cfg, rank, world, local):
     p_mean = float(np.mean(pairs)) if pairs else 0.0
     if dist:
         t = torch.tensor([p_mean * n_mine, float(n_mine)], dtype=torch.float64, device=dev)
-        dist.all_reduce(t)
+        reduce_(t)
         p_mean = float(t[0] / max(t[1], 1.0))
     med = {k: statistics.median(d[k] for d in stage_ms) for k in stage_ms[0]}
     hbm, peak_kind = peaks()
@@ -495,7 +513,7 @@ def run_ours(args, cfg, rank, world, local):
         rp_s = time.perf_counter() - w0
         if dist:
             t = torch.tensor([ems, rms, rp_s], dtype=torch.float64, device=dev)
-            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            reduce_(t, op=dist.ReduceOp.MAX)
             ems, rms, rp_s = (float(v) for v in t.tolist())
         e2e = {"value": world * k_e2e / (ems * 1e-3), "unit": "frames/s",
                "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
