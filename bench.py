@@ -429,56 +429,67 @@ def run_ours(args, cfg, rank, world, local):
     falg = frame_algorithmic_bytes(n, k_sh, p_mean, cfg["w"], cfg["h"])
 
     # e2e legs (per rank; aggregated over ranks)
-    e2e = e2e_res = e2e_rp = None
+    e2e = e2e_frame = e2e_res = e2e_rp = None
     if not args.no_e2e and n_mine:
-        img_h = torch.empty_like(rast.pixels, device="cpu").pin_memory()
-        load_h = torch.empty_like(rast.load, device="cpu").pin_memory()
         src = [host.centers, host.scales, host.rotations, host.opacities, host.sh]
         dst = [ds.centers, ds.scales, ds.rotations, ds.opacities, ds.sh]
         h2d = host.nbytes()
-        d2h = img_h.numel() * 4 + load_h.numel() * 4
-        k_e2e = max(3, min(args.steps, 20))
-        # (1) drop-in frame: the scene copied from pinned host memory every frame,
-        # image + load map back to pinned host memory.  Two device copies of the
-        # scene: step s+1's H2D copy (copy stream) overlaps step s's frame.
+        slot_h = [(torch.empty_like(r.pixels, device="cpu").pin_memory(),
+                   torch.empty_like(r.load, device="cpu").pin_memory()) for r in rasts]
+        d2h_frame = slot_h[0][0].numel() * 4 + slot_h[0][1].numel() * 4
+        k_e2e = max(3, min(args.steps, 10))
+        # two device copies of the scene: step s+1's H2D copy (copy stream)
+        # overlaps step s's frames; every step still moves its own scene in
         dst2 = [t.clone() for t in dst]
         ds2 = ab.DeviceScene(*dst2, sh_degree=ds.sh_degree)
-        n_e2e_views = min(n_mine, 4)
-        eg = [[rast.capture(d, cams[mine[j]], mode=cfg["mode"]) for j in range(n_e2e_views)] for d in (ds, ds2)]
-        bufs = [dst, dst2]
+        scenes, bufs = (ds, ds2), (dst, dst2)
         cstream = torch.cuda.Stream(dev)
         ready = [torch.cuda.Event(), torch.cuda.Event()]
         free = [torch.cuda.Event(), torch.cuda.Event()]
-        for it in range(2):
-            for a_, b_ in zip(dst, src):
-                a_.copy_(b_, non_blocking=True)
-            eg[0][0].replay()
-        torch.cuda.synchronize(dev)
-        if dist:
-            dist.barrier()
-        a0, a1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        a0.record(stream)
-        cstream.wait_event(a0)
-        for s_ in range(k_e2e):
-            bb = s_ % 2
-            with torch.cuda.stream(cstream):
-                if s_ >= 2:
-                    cstream.wait_event(free[bb])
-                for a_, b_ in zip(bufs[bb], src):
-                    a_.copy_(b_, non_blocking=True)
-                ready[bb].record(cstream)
-            stream.wait_event(ready[bb])
-            eg[bb][s_ % n_e2e_views].replay()
-            img_h.copy_(rast.pixels, non_blocking=True)
-            load_h.copy_(rast.load, non_blocking=True)
-            free[bb].record(stream)
-        a1.record(stream)
-        torch.cuda.synchronize(dev)
-        ems = a0.elapsed_time(a1)
-        # (2) resident scene (serving): per step a new camera through the C-ABI
-        # frame call (Rasterizer.launch, no graph) on one of the in-flight slots
-        slot_h = [(torch.empty_like(r.pixels, device="cpu").pin_memory(),
-                   torch.empty_like(r.load, device="cpu").pin_memory()) for r in rasts]
+
+        def e2e_run(steps: int, views_per_step: int) -> float:
+            """Per step: the scene H2D from pinned host memory, `views_per_step`
+            of this rank's views through the C-ABI frame call (Rasterizer.launch,
+            no graph) on the in-flight slots, each frame's image + load map D2H
+            to pinned host memory."""
+            torch.cuda.synchronize(dev)
+            if dist:
+                dist.barrier()
+            a0, a1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a0.record(stream)
+            cstream.wait_event(a0)
+            j = 0
+            for s_ in range(steps):
+                bb = s_ % 2
+                with torch.cuda.stream(cstream):
+                    if s_ >= 2:
+                        cstream.wait_event(free[bb])
+                    for x_, y_ in zip(bufs[bb], src):
+                        x_.copy_(y_, non_blocking=True)
+                    ready[bb].record(cstream)
+                for st in streams:
+                    st.wait_event(ready[bb])
+                for _ in range(views_per_step):
+                    k = j % n_fly
+                    rasts[k].launch(scenes[bb], cams[mine[j % n_mine]], mode=cfg["mode"], stream=streams[k])
+                    with torch.cuda.stream(streams[k]):
+                        slot_h[k][0].copy_(rasts[k].pixels, non_blocking=True)
+                        slot_h[k][1].copy_(rasts[k].load, non_blocking=True)
+                    j += 1
+                for st in streams:
+                    ev = torch.cuda.Event()
+                    ev.record(st)
+                    stream.wait_event(ev)
+                free[bb].record(stream)
+            a1.record(stream)
+            torch.cuda.synchronize(dev)
+            return a0.elapsed_time(a1)
+
+        e2e_run(2, n_mine)   # warm-up
+        ems = e2e_run(k_e2e, n_mine)          # the bench's step: this rank's V/R views per scene upload
+        fms = e2e_run(k_e2e, 1)               # one frame per scene upload
+        # resident scene (serving): per step a new camera through the C-ABI
+        # frame call on one of the in-flight slots, image+load map back
         torch.cuda.synchronize(dev)
         b0, b1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         b0.record(stream)
@@ -498,9 +509,8 @@ def run_ours(args, cfg, rank, world, local):
         b1.record(stream)
         torch.cuda.synchronize(dev)
         rms = b0.elapsed_time(b1)
-        # (3) the literal drop-in call: run_pipeline(pinned host scene, camera)
-        # -> PipelineResult; synchronous, wall clock per call (upload, frame,
-        # stage events, result copies)
+        # the literal drop-in call: run_pipeline(pinned host scene, camera) ->
+        # PipelineResult; synchronous, wall clock per call
         ab.run_pipeline(host, cams[mine[0]], mode=cfg["mode"])
         torch.cuda.synchronize(dev)
         if dist:
@@ -512,20 +522,25 @@ def run_ours(args, cfg, rank, world, local):
             _ = res.image.pixels.cpu()
         rp_s = time.perf_counter() - w0
         if dist:
-            t = torch.tensor([ems, rms, rp_s], dtype=torch.float64, device=dev)
+            t = torch.tensor([ems, fms, rms, rp_s], dtype=torch.float64, device=dev)
             reduce_(t, op=dist.ReduceOp.MAX)
-            ems, rms, rp_s = (float(v) for v in t.tolist())
-        e2e = {"value": world * k_e2e / (ems * 1e-3), "unit": "frames/s",
-               "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
-               "path": "frame via the C-ABI with the scene copied from pinned host memory every step and "
-                       "image+load map copied back (run_pipeline semantics); double-buffered device scene: "
-                       "step s+1's H2D copy overlaps step s's frame"}
+            ems, fms, rms, rp_s = (float(v) for v in t.tolist())
+        e2e = {"value": views * k_e2e / (ems * 1e-3), "unit": "frames/s",
+               "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h_frame * n_mine,
+               "path": "per step (as in value: this rank's views of the batch): the scene H2D from pinned "
+                       "host memory, every view through the C-ABI frame call (Rasterizer.launch, no graph), "
+                       "each image + load map D2H to pinned host memory; double-buffered device scene (step "
+                       "s+1's upload overlaps step s's frames)"}
+        e2e_frame = {"value": world * k_e2e / (fms * 1e-3), "unit": "frames/s",
+                     "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h_frame,
+                     "path": "the same with one view per scene upload (run_pipeline semantics: every frame "
+                             "re-sends its scene)"}
         e2e_res = {"value": world * n_res / (rms * 1e-3), "unit": "frames/s",
-                   "h2d_bytes_per_step": ctypes.sizeof(_lib.Camera_t), "d2h_bytes_per_step": d2h,
+                   "h2d_bytes_per_step": ctypes.sizeof(_lib.Camera_t), "d2h_bytes_per_step": d2h_frame,
                    "path": "resident scene; per step Rasterizer.launch with a new camera (C-ABI call, "
                            "no graph) on one of the in-flight slots, image+load map copied to pinned host"}
         e2e_rp = {"value": world * k_rp / rp_s, "unit": "frames/s", "h2d_bytes_per_step": h2d,
-                  "d2h_bytes_per_step": img_h.numel() * 4,
+                  "d2h_bytes_per_step": slot_h[0][0].numel() * 4,
                   "path": "paper_2409_08669_b200.run_pipeline(pinned host DeviceScene, camera) per frame, "
                           "synchronous, wall clock (includes the scene upload, stage events, result copies)"}
 
@@ -589,6 +604,7 @@ def run_ours(args, cfg, rank, world, local):
         }
         if e2e:
             line["e2e"] = e2e
+            line["e2e_frame_upload"] = e2e_frame
             line["e2e_resident"] = e2e_res
             line["e2e_run_pipeline"] = e2e_rp
         if cpu:
