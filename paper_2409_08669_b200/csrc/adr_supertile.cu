@@ -42,6 +42,11 @@
 
 namespace adr {
 
+// adr_depthsort.cu
+size_t depth_sort_scratch(int64_t n);
+int32_t depth_sort_onesweep(const uint32_t* dkey, int64_t n, const DepthPlan& dp, const uint2* gpack, uint4* rinfo,
+                            void* scratch, size_t scratch_bytes, cudaStream_t st);
+
 namespace {
 
 constexpr int kStSide = 8;            // supertile side in tiles
@@ -715,8 +720,7 @@ size_t supertile_scratch(int64_t n, int64_t cap, int32_t tx, int32_t ty) {
     const int64_t icap = st_items_cap(cap, S);
     size_t s = 0;
     s += align_up(16 * (size_t)n);               // rinfo
-    s += radix_scratch_bytes<uint32_t, uint32_t>(n);
-    s += 2 * align_up(4 * (size_t)n);            // depth-sort key / value outputs (unused by MODE 3)
+    s += depth_sort_scratch(n);
     s += align_up(4 * (size_t)(n1p * S));        // H1
     s += 3 * align_up(4 * (size_t)(S + 1));      // total, pstart, iend
     s += align_up(2 * (size_t)(icap / kChunk + 1));  // cmap
@@ -749,9 +753,8 @@ int32_t frame_binning_supertile(const FrameBinning& fb, cudaStream_t st) {
     const int64_t n2max = icap / kChunk;
     Carver cv(fb.scratch, fb.scratch_bytes);
     uint4* rinfo = cv.take<uint4>(n);
-    void* rs1 = cv.take<char>((int64_t)radix_scratch_bytes<uint32_t, uint32_t>(n));
-    uint32_t* skey = cv.take<uint32_t>(n);
-    uint32_t* sval = cv.take<uint32_t>(n);
+    const size_t ds_bytes = depth_sort_scratch(n);
+    void* ds_scratch = cv.take<char>((int64_t)ds_bytes);
     uint32_t* H1 = cv.take<uint32_t>(g.n1p * g.S);
     StCtl c;
     c.total = cv.take<uint32_t>(g.S + 1);
@@ -772,19 +775,16 @@ int32_t frame_binning_supertile(const FrameBinning& fb, cudaStream_t st) {
     int64_t* ctr = fb.counters;   // [0]=P, [1]=culled, [2]=M, [3]=P clamped, [6]=truncated, [7]=tickets
     c.ticket = reinterpret_cast<unsigned int*>(ctr + 7);
 
-    // depth-rank order; the last pass writes rinfo[rank] = {index, depth bits, rect}
-    SortExtra dx;
-    dx.mode = 3;
-    dx.gsrc = fb.gpack;
-    dx.rinfo = rinfo;
-    if (fb.kminmax && fb.plan_mm) {   // key-range plan, reduced by extra blocks of pass 0's upsweep
-        dx.dp.plan = fb.plan_mm;
-        dx.dp.plan_out = fb.plan_mm;
-        dx.dp.kminmax = fb.kminmax;
-        dx.dp.nkb = ceil_div(n, 128);
+    // depth-rank order (onesweep, adr_depthsort.cu); the last pass writes
+    // rinfo[rank] = {index, depth bits, rect}
+    DepthPlan dp;
+    if (fb.kminmax && fb.plan_mm) {   // key-range plan from the preprocess's per-block extrema
+        dp.plan = fb.plan_mm;
+        dp.plan_out = fb.plan_mm;
+        dp.kminmax = fb.kminmax;
+        dp.nkb = ceil_div(n, 128);
     }
-    int32_t rc = radix_sort<uint32_t, uint32_t>(fb.dkey, nullptr, skey, sval, nullptr, n, 32, rs1,
-                                                radix_scratch_bytes<uint32_t, uint32_t>(n), st, dx);
+    int32_t rc = depth_sort_onesweep(fb.dkey, n, dp, fb.gpack, rinfo, ds_scratch, ds_bytes, st);
     if (rc) return rc;
     if (fb.ev_after_scan) ADR_CUDA_TRY(cudaEventRecord(fb.ev_after_scan, st));   // stage "depth sort"
     // L1: ranks -> supertile items
