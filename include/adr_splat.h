@@ -171,6 +171,13 @@ int32_t adr_selftest_exp(uint64_t* d_result, void* stream);
  * tests/golden/make_exp_exhaustive.py computes over np.exp(float32). */
 int32_t adr_exp_checksum(uint64_t lo, uint64_t hi, uint64_t* d_out, void* stream);
 
+/* The PLY loader's float64 activations (test infrastructure): over every
+ * non-NaN float32 bit pattern u in [lo, hi) widened to float64, the sum of
+ * (bits(f(u)) + 1) * (u * 0x9E3779B97F4A7C15 | 1) mod 2^64 with f = np.exp
+ * (kind 0) or scipy.special.expit (kind 1) as adr_ply_activate evaluates
+ * them; tests/golden/make_exp64_exhaustive.py sums numpy / scipy. */
+int32_t adr_exp64_checksum(int32_t kind, uint64_t lo, uint64_t hi, uint64_t* d_out, void* stream);
+
 /* Render self-check (test infrastructure, no reference counterpart).  With
  * enable != 0 the following frames launch the counting instantiation of the
  * tile blend, which iterates each warp's plain bounding box and counts every
@@ -181,6 +188,24 @@ int32_t adr_exp_checksum(uint64_t lo, uint64_t hi, uint64_t* d_out, void* stream
  * [2] = warp iterations the mask removes, [6] = batches + 1e9 x unsafe
  * removals (must stay < 1e9). */
 int32_t adr_render_selfcheck(int32_t enable, unsigned long long* host_out);
+
+/* ------------------------------------------------------------ PLY ingest */
+
+/* load_ply (sb/scene.py:316-398), device half: activates rows
+ * [row0, row0 + rows) of the float32 property matrix (d_raw = row row0's
+ * first property, n_props floats per row, file order) into the float64
+ * scene *out (dtype ADR_F64, out->n = all rows): centers = (x, y, z),
+ * scales = np.exp(scale_*), rotations = rot / np.linalg.norm(rot),
+ * opacities = scipy expit(opacity), sh = (f_dc, f_rest) gathered to (K, 3),
+ * bit-identical to the reference's numpy / scipy arithmetic.  cols (host,
+ * 11 + 3K entries): the property column of x, y, z, scale_0..2, rot_0..3,
+ * opacity, then each SH coefficient in (k, channel) order.  d_status
+ * (device, 2 int64, reset to INT64_MAX by adr_ply_status_reset) receives the
+ * smallest row with a non-finite property (scene.py:370-373) and with a
+ * quaternion norm < 1e-12 (scene.py:388-391); the caller raises from them. */
+int32_t adr_ply_status_reset(int64_t* d_status, void* stream);
+int32_t adr_ply_activate(const float* d_raw, int64_t row0, int64_t rows, int32_t n_props,
+                         const int32_t* cols, const adr_scene* out, int64_t* d_status, void* stream);
 
 /* ----------------------------------------------- brute-force reference path */
 

@@ -559,3 +559,164 @@ uint64_t orc_exp_checksum(uint64_t lo, uint64_t hi) {
     }
     return total;
 }
+
+/* ------------------------------------------------------------------------ */
+/* float64 exp of the PLY loader (scene.py:385-386), test infrastructure.    */
+/* numpy 2.3.5's np.exp(float64) on this AVX512_SKX host is Intel SVML's     */
+/* __svml_exp8_ha (vendored in numpy); scipy's expit(x) is                    */
+/* 1 / (1 + exp(-x)) with glibc 2.39's exp (its FMA variant).  Both are      */
+/* restated operation by operation from the disassembly of those library     */
+/* builds; the tables come from tools/gen_exp64_tables.py (first principles). */
+/* ------------------------------------------------------------------------ */
+
+#include "../paper_2409_08669_b200/csrc/adr_exp64_tab.h"
+
+static const uint64_t k_s16_hi[16] = ADR_SVML16_HI;
+static const uint64_t k_s16_lo[16] = ADR_SVML16_LO;
+static const uint64_t k_s64[128] = ADR_SVML64_HILO;
+static const uint64_t k_g128[256] = ADR_GLIBC128;
+
+static inline double d_from_bits(uint64_t u) { double d; memcpy(&d, &u, 8); return d; }
+static inline uint64_t bits_from_d(double d) { uint64_t u; memcpy(&u, &d, 8); return u; }
+
+/* SVML's scalar path for |x| >= 0x1.61da04cbafe44p+9 and +-inf (plain SSE
+ * arithmetic, no FMA): 2^(j/64) table, degree-5 polynomial, and a split
+ * rounding for subnormal results. */
+static double svml_exp_rare(double x) {
+    const uint64_t ux = bits_from_d(x);
+    if (((ux >> 52) & 0x7ff) == 0x7ff) return ux == 0xfff0000000000000ull ? 0.0 : x * x;
+    if (x > 0x1.62e42fefa39efp+9) return 0x1.fffffffffffffp+1023 * 0x1.fffffffffffffp+1023;
+    if (x < -0x1.74910d52d3051p+9) return 0x1.0000000000001p-1022 * 0x1.0000000000001p-1022;
+    const double t1 = x * 0x1.71547652b82fep+6 + 0x1.8p52;   /* two roundings (no contraction) */
+    const uint32_t n32 = (uint32_t)bits_from_d(t1);
+    const uint32_t j = n32 & 63u, k = n32 >> 6;
+    const double nf = t1 - 0x1.8p52;
+    double r = x - nf * 0x1.62e42fefa0000p-7;
+    r = r - nf * 0x1.cf79abc9e3b3ap-46;
+    const double hi = d_from_bits(k_s64[2 * j]), lo = d_from_bits(k_s64[2 * j + 1]);
+    double p = 0x1.6c16a1c2a3ffdp-10 * r + 0x1.111123aaf20d3p-7;
+    p = p * r + 0x1.5555555558fccp-5;
+    p = p * r + 0x1.55555555548f8p-3;
+    p = p * r + 0x1.0p-1;
+    p = p * r * r + r;
+    p = (p + lo) * hi;
+    if (!(x < -0x1.6232bdd7abcd2p+9)) {
+        uint32_t e = (k + 0x3ffu) & 0x7ffu;
+        const double y = p + hi;
+        if (e > 0x7fe) {
+            e = (e - 1) & 0x7ffu;
+            return y * d_from_bits((uint64_t)e << 52) * 2.0;
+        }
+        return y * d_from_bits((uint64_t)e << 52);
+    }
+    const uint32_t e = (k + 0x43bu) & 0x7ffu;          /* scaled by 2^60 */
+    const double sc = d_from_bits((uint64_t)e << 52);
+    const double a = p * sc, b = sc * hi, s = b + a;
+    if (e <= 0x32) return s * 0x1p-60;
+    const double l = (b - s) + a;
+    const double c = s * 0x1.8p32, h = (s + c) - c;
+    const double el = l + (s - h);
+    return h * 0x1p-60 + el * 0x1p-60;
+}
+
+/* np.exp(float64) = __svml_exp8_ha: z = RZ(x / ln2 + shifter) puts
+ * floor16(x / ln2) and its 1/16 index in z's low bits; r = x - N ln2 (two
+ * FMA steps); exp(r) by a degree-6 polynomial; result scaled by 2^floor(N). */
+double orc_exp_svml(double x) {
+    const double shifter = 0x1.8000000003ff0p+48;
+    if (fabs(x) >= 0x1.61da04cbafe44p+9) return svml_exp_rare(x);
+    double z = fma(x, 0x1.71547652b82fep+0, shifter);
+    /* round toward zero (z > 0): step down when RN rounded up */
+    if (fma(x, 0x1.71547652b82fep+0, -(z - shifter)) < 0.0) z = d_from_bits(bits_from_d(z) - 1);
+    const uint32_t j = (uint32_t)(bits_from_d(z) & 15u);
+    const double n = z - shifter;
+    double r = fma(-n, 0x1.62e42fefa39efp-1, x);
+    r = fma(-n, 0x1.abc9e3b39803fp-56, r);
+    r = d_from_bits(bits_from_d(r) & 0xbfffffffffffffffull);
+    const double r2 = r * r;
+    double a = fma(0x1.7411836940c04p-10, r, 0x1.1101cbbc265c0p-7);
+    const double b = fma(0x1.55557242d68fep-5, r, 0x1.5555553939732p-3);
+    const double c = fma(0x1.000000000d008p-1, r, 0x1.fffffffffff70p-1);
+    a = fma(r2, a, b);
+    a = fma(r2, a, c);
+    const double hi = d_from_bits(k_s16_hi[j]), lo = d_from_bits(k_s16_lo[j]);
+    const double v = fma(a, r, lo);
+    const double m = fma(hi, v, hi);
+    return ldexp(m, (int)floor(n));   /* vscalefpd; normal for this range */
+}
+
+/* glibc 2.39 exp (sysdeps/ieee754/dbl-64/e_exp.c design, FMA build). */
+double orc_exp_glibc(double x) {
+    const uint64_t ux = bits_from_d(x);
+    uint32_t abstop = (uint32_t)(ux >> 52) & 0x7ff;
+    if (abstop - 0x3c9u >= 0x3fu) {
+        if ((int32_t)(abstop - 0x3c9u) < 0) return 1.0 + x;
+        if (abstop >= 0x409) {
+            if (ux == 0xfff0000000000000ull) return 0.0;
+            if (abstop == 0x7ff) return 1.0 + x;
+            return (ux >> 63) ? 0x1p-767 * 0x1p-767 : 0x1p769 * 0x1p769;
+        }
+        abstop = 0;   /* |x| in [512, 1024): the scaled special case */
+    }
+    double kd = fma(x, 0x1.71547652b82fep+7, 0x1.8p52);
+    const uint64_t ki = bits_from_d(kd);
+    kd -= 0x1.8p52;
+    double r = fma(kd, -0x1.62e42fefa0000p-8, x);
+    r = fma(kd, -0x1.cf79abc9e3b3ap-47, r);
+    const uint32_t idx = 2u * (uint32_t)(ki & 127u);
+    const uint64_t top = ki << 45;
+    const double tail = d_from_bits(k_g128[idx]);
+    uint64_t sbits = k_g128[idx + 1] + top;
+    const double a = fma(r, 0x1.555555555543cp-3, 0x1.ffffffffffdbdp-2);
+    const double t = r + tail;
+    const double r2 = r * r;
+    const double b = fma(r, 0x1.1111167a4d017p-7, 0x1.55555cf172b91p-5);
+    const double t2 = fma(a, r2, t);
+    const double tmp = fma(r2 * r2, b, t2);
+    if (abstop == 0) {
+        if ((ki & 0x80000000ull) == 0) {
+            sbits -= 1009ull << 52;
+            const double scale = d_from_bits(sbits);
+            return 0x1p1009 * fma(scale, tmp, scale);
+        }
+        sbits += 1022ull << 52;
+        const double scale = d_from_bits(sbits);
+        const double st = scale * tmp;
+        double y = scale + st;
+        if (y < 1.0) {
+            const double lo = (scale - y) + st;
+            const double hi = 1.0 + y;
+            const double l2 = ((1.0 - hi) + y) + lo;
+            y = (hi + l2) - 1.0;
+            if (y == 0.0) y = 0.0;
+        }
+        return y * 0x1p-1022;
+    }
+    const double scale = d_from_bits(sbits);
+    return fma(scale, tmp, scale);
+}
+
+/* scipy.special.expit(float64) (scene.py:385). */
+double orc_expit(double x) { return 1.0 / (1.0 + orc_exp_glibc(-x)); }
+
+/* Exhaustive pin over float32 inputs widened to float64 (a PLY stores
+ * float32): H = sum over non-NaN bit patterns u in [lo, hi) of
+ * (bits(f(u)) + 1) * (u * 0x9E3779B97F4A7C15 | 1) mod 2^64; kind 0 = np.exp,
+ * 1 = expit.  tests/golden/make_exp64_exhaustive.py sums numpy / scipy. */
+uint64_t orc_exp64_checksum(int32_t kind, uint64_t lo, uint64_t hi) {
+    uint64_t total = 0;
+#pragma omp parallel for reduction(+ : total) schedule(dynamic, 16)
+    for (int64_t c = (int64_t)(lo >> 20); c < (int64_t)((hi + 0xfffff) >> 20); ++c) {
+        uint64_t s = 0;
+        const uint64_t a = (uint64_t)c << 20, b = ((uint64_t)c + 1) << 20;
+        for (uint64_t u = a < lo ? lo : a; u < (b < hi ? b : hi); ++u) {
+            const uint32_t ub = (uint32_t)u;
+            if ((ub & 0x7fffffffu) > 0x7f800000u) continue;
+            const double x = (double)f_from_bits(ub);
+            const double y = kind == 0 ? orc_exp_svml(x) : orc_expit(x);
+            s += (bits_from_d(y) + 1u) * ((u * 0x9E3779B97F4A7C15ull) | 1u);
+        }
+        total += s;
+    }
+    return total;
+}

@@ -69,6 +69,11 @@ def lib():
         _lib.orc_exp_np.argtypes = [ctypes.c_float]
         _lib.orc_exp_checksum.restype = ctypes.c_uint64
         _lib.orc_exp_checksum.argtypes = [ctypes.c_uint64, ctypes.c_uint64]
+        for fn in ("orc_exp_svml", "orc_exp_glibc", "orc_expit"):
+            getattr(_lib, fn).restype = ctypes.c_double
+            getattr(_lib, fn).argtypes = [ctypes.c_double]
+        _lib.orc_exp64_checksum.restype = ctypes.c_uint64
+        _lib.orc_exp64_checksum.argtypes = [ctypes.c_int32, ctypes.c_uint64, ctypes.c_uint64]
         _lib.orc_log.restype = ctypes.c_double
         _lib.orc_log.argtypes = [ctypes.c_double]
         _lib.orc_inclusive_sum.restype = ctypes.c_int32

@@ -22,7 +22,7 @@ from .refrender import render_reference
 from .render import ALPHA_CLAMP, TERMINATION_THRESHOLD, Image, LoadMap, render
 from .scene import (Camera, DeviceScene, Gaussian3D, Scene, SceneArrays, SyntheticSpec,
                     generate_synthetic, synthetic_arrays)
-from .scene_io import (SceneDiagnostic, load_json, load_ply, load_ply_arrays, load_scene,
+from .scene_io import (SceneDiagnostic, load_json, load_ply, load_ply_arrays, load_ply_device, load_scene,
                        load_scene_arrays, normalize_quaternion, save_json, save_ply, save_scene,
                        validate_scene)
 from .tiling import (TILE_SIZE, TileGrid, TilePairList, TileRect, build_pairs,
@@ -38,7 +38,7 @@ __all__ = [
     "LoadMap", "LoadStats", "PipelineResult", "Projection", "Rasterizer", "RenderStats", "Scene",
     "SceneArrays", "SceneFormatError", "SceneValidationError", "SyntheticSpec", "TileGrid",
     "TilePairList", "TileRect", "build_pairs", "SceneDiagnostic", "load_json", "load_ply",
-    "load_ply_arrays", "load_scene", "load_scene_arrays", "normalize_quaternion", "save_json",
+    "load_ply_arrays", "load_ply_device", "load_scene", "load_scene_arrays", "normalize_quaternion", "save_json",
     "save_ply", "save_scene", "validate_scene", "DEFAULT_WEIGHTS", "BalanceStepResult", "LossWeights",
     "l1_loss", "render_reference", "CullExtent", "EllipseCoefficients", "ProjectedGaussian",
     "aabb_extents", "bounding_box_halfwidths", "bounding_circle_radius", "build_covariance3d",

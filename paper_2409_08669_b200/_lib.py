@@ -31,7 +31,8 @@ EXPORTED = (
     "adr_abi_version", "adr_last_error", "adr_kernel_launches", "adr_device_sm_count", "adr_preprocess",
     "adr_touched_counts", "adr_inclusive_sum_scratch_bytes", "adr_inclusive_sum",
     "adr_duplicate_with_keys", "adr_sort_pairs_scratch_bytes", "adr_sort_pairs",
-    "adr_identify_tile_ranges", "adr_render", "adr_exp_np_f32", "adr_selftest_exp", "adr_exp_checksum", "adr_render_selfcheck",
+    "adr_identify_tile_ranges", "adr_render", "adr_exp_np_f32", "adr_selftest_exp", "adr_exp_checksum", "adr_exp64_checksum", "adr_render_selfcheck",
+    "adr_ply_status_reset", "adr_ply_activate",
     "adr_frame_scratch_bytes", "adr_frame_record_offset", "adr_render_frame", "adr_image_loss_scratch_bytes", "adr_image_losses",
     "adr_render_reference_scratch_bytes", "adr_render_reference",
 )
@@ -116,6 +117,9 @@ def lib() -> ctypes.CDLL:
             "adr_selftest_exp": (i32, [vp, vp]),
             "adr_render_selfcheck": (i32, [i32, vp]),
             "adr_exp_checksum": (i32, [ctypes.c_uint64, ctypes.c_uint64, vp, vp]),
+            "adr_exp64_checksum": (i32, [i32, ctypes.c_uint64, ctypes.c_uint64, vp, vp]),
+            "adr_ply_status_reset": (i32, [vp, vp]),
+            "adr_ply_activate": (i32, [vp, i64, i64, i32, P(i32), P(Scene_t), vp, vp]),
             "adr_frame_scratch_bytes": (sz, [i64, i32, i32, i64]),
             "adr_frame_record_offset": (sz, [i64, i32, i32, i64]),
             "adr_render_frame": (i32, [P(Scene_t), P(Camera_t), i32, dbl, dbl, dbl,

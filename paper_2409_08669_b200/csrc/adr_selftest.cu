@@ -9,6 +9,7 @@
 #include "adr_common.cuh"
 #include "adr_f32x2.cuh"
 #include "adr_scan.cuh"
+#include "adr_exp64.cuh"
 
 namespace adr {
 namespace {
@@ -53,6 +54,24 @@ __global__ void k_exp_checksum(uint64_t lo, uint64_t hi, unsigned long long* out
     if ((threadIdx.x & 31) == 0) atomicAdd(out, (unsigned long long)s);
 }
 
+// The PLY loader's float64 activations over every non-NaN float32 input u
+// in [lo, hi) widened to float64: H = sum of (bits(f(u)) + 1) *
+// (u * 0x9E3779B97F4A7C15 | 1) mod 2^64, kind 0 = np.exp (exp_svml),
+// 1 = scipy expit (expit_glibc); tests/golden/make_exp64_exhaustive.py.
+__global__ void k_exp64_checksum(int32_t kind, uint64_t lo, uint64_t hi, unsigned long long* out) {
+    uint64_t s = 0;
+    const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+    for (uint64_t u = lo + (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; u < hi; u += stride) {
+        const uint32_t ub = (uint32_t)u;
+        if ((ub & 0x7fffffffu) > 0x7f800000u) continue;
+        const double x = (double)__uint_as_float(ub);
+        const double y = kind == 0 ? exp_svml(x) : expit_glibc(x);
+        s += (ubits(y) + 1u) * ((u * 0x9E3779B97F4A7C15ull) | 1u);
+    }
+    s = warp_sum(s);
+    if ((threadIdx.x & 31) == 0) atomicAdd(out, (unsigned long long)s);
+}
+
 }  // namespace
 }  // namespace adr
 
@@ -73,6 +92,16 @@ int32_t adr_exp_checksum(uint64_t lo, uint64_t hi, uint64_t* d_out, void* stream
     ADR_CUDA_TRY(cudaMemsetAsync(d_out, 0, sizeof(uint64_t), st));
     if (hi <= lo) return ADR_OK;
     k_exp_checksum<<<148 * 8, 256, 0, st>>>(lo, hi, reinterpret_cast<unsigned long long*>(d_out));
+    ADR_LAUNCH_CHECK();
+    return ADR_OK;
+}
+
+int32_t adr_exp64_checksum(int32_t kind, uint64_t lo, uint64_t hi, uint64_t* d_out, void* stream) {
+    if (kind != 0 && kind != 1) return fail(ADR_ERR_VALUE, "adr_exp64_checksum: kind must be 0 or 1");
+    cudaStream_t st = as_stream(stream);
+    ADR_CUDA_TRY(cudaMemsetAsync(d_out, 0, sizeof(uint64_t), st));
+    if (hi <= lo) return ADR_OK;
+    k_exp64_checksum<<<148 * 8, 256, 0, st>>>(kind, lo, hi, reinterpret_cast<unsigned long long*>(d_out));
     ADR_LAUNCH_CHECK();
     return ADR_OK;
 }

@@ -165,3 +165,43 @@ def test_cli_render_compare_loadmap_bench_on_gpu(tmp_path, oracle):
     rows = list(csv.DictReader(open(csvp)))
     assert list(rows[0].keys()) == cli.BENCH_COLUMNS and len(rows) == 2
     assert int(rows[1]["pairs"]) == len(ref["keys"]) and float(rows[1]["fps"]) > 0
+
+
+@pytest.mark.parametrize("name", ["sh3_extreme", "sh0_shuffled", "sh1_small", "sh2_reversed"])
+def test_ply_cases_host_path_matches_reference_digests(name, tmp_path):
+    """The deterministic checkpoints of tests/ply_cases.py (extreme logits and
+    log-scales across the exp / expit special-case thresholds, shuffled and
+    extra properties) load to the same arrays as the real splatbench's
+    load_ply (tests/golden/ply_digests.json); the device ingest is checked
+    against the same digests in tests/test_gpu_ply.py."""
+    import json
+
+    import paper_2409_08669_b200 as ab
+    from ply_cases import write_case
+
+    want = json.loads((GOLDEN / "ply_digests.json").read_text())[name]
+    path = write_case(tmp_path, name)
+    assert hashlib.sha256(path.read_bytes()).hexdigest() == want["file_sha256"]
+    with np.errstate(over="ignore"):
+        arrays, _ = ab.load_ply_arrays(path)
+    for f in ("centers", "scales", "rotations", "opacities", "sh"):
+        got = hashlib.sha256(np.ascontiguousarray(getattr(arrays, f), dtype=np.float64).tobytes()).hexdigest()
+        assert got == want[f], f
+
+
+def test_ply_device_columns_follow_the_reference_layout():
+    """adr_ply_activate's column map: x y z, scale, rot, opacity, then SH in
+    (k, channel) order with f_rest channel-major (sb/scene.py:380-384)."""
+    from paper_2409_08669_b200.scene_io import PlySchema
+
+    schema = PlySchema(2)
+    names = list(schema.names)[::-1]
+    index = {nm: i for i, nm in enumerate(names)}
+    cols = schema.device_columns(index)
+    assert cols.dtype == np.int32 and cols.size == 11 + 3 * 9
+    named = [names[c] for c in cols]
+    assert named[:11] == ["x", "y", "z", "scale_0", "scale_1", "scale_2", "rot_0", "rot_1", "rot_2", "rot_3",
+                          "opacity"]
+    assert named[11:14] == ["f_dc_0", "f_dc_1", "f_dc_2"]
+    assert named[14:17] == ["f_rest_0", "f_rest_8", "f_rest_16"]   # k = 1: channel c at c * (K - 1)
+    assert named[-3:] == ["f_rest_7", "f_rest_15", "f_rest_23"]
