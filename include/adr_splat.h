@@ -193,7 +193,8 @@ int32_t adr_render_selfcheck(int32_t enable, unsigned long long* host_out);
 
 /* load_ply (sb/scene.py:316-398), device half: activates rows
  * [row0, row0 + rows) of the float32 property matrix (d_raw = row row0's
- * first property, n_props floats per row, file order) into the float64
+ * first property, 16-byte aligned, n_props <= 1536 floats per row, file
+ * order) into the float64
  * scene *out (dtype ADR_F64, out->n = all rows): centers = (x, y, z),
  * scales = np.exp(scale_*), rotations = rot / np.linalg.norm(rot),
  * opacities = scipy expit(opacity), sh = (f_dc, f_rest) gathered to (K, 3),
