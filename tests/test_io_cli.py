@@ -205,3 +205,30 @@ def test_ply_device_columns_follow_the_reference_layout():
     assert named[11:14] == ["f_dc_0", "f_dc_1", "f_dc_2"]
     assert named[14:17] == ["f_rest_0", "f_rest_8", "f_rest_16"]   # k = 1: channel c at c * (K - 1)
     assert named[-3:] == ["f_rest_7", "f_rest_15", "f_rest_23"]
+
+
+def test_ply_source_memory_maps_large_files(tmp_path):
+    """load_ply_device's host side: a large file is memory-mapped (header from
+    a 1 MB probe, same body offset as the whole blob), and a header whose
+    end marker lies beyond the probe is still found (the reference searches
+    the whole file, sb/scene.py:327)."""
+    from paper_2409_08669_b200.scene_io import _HEADER_PROBE, _parse_ply_header, _ply_source
+    from ply_cases import make_raw, write_ply
+
+    names, raw = make_raw("sh1_small")
+    big = np.concatenate([raw] * (2 * _HEADER_PROBE // raw.nbytes + 1))
+    p = write_ply(tmp_path / "big.ply", names, big)
+    head, whole = _ply_source(p)
+    assert len(head) == _HEADER_PROBE and isinstance(whole, np.memmap)
+    blob = p.read_bytes()
+    assert _parse_ply_header(head, p)[1:] == _parse_ply_header(blob, p)[1:]
+    body = _parse_ply_header(head, p)[3]
+    got = np.frombuffer(whole, dtype="<f4", count=big.size, offset=body).reshape(big.shape)
+    assert np.array_equal(got.view(np.uint32), big.view(np.uint32))
+    # a comment-padded header longer than the probe
+    pad = b"ply\nformat binary_little_endian 1.0\n" + b"comment x\n" * (_HEADER_PROBE // 10 + 10)
+    q = tmp_path / "long_header.ply"
+    q.write_bytes(pad + p.read_bytes()[len(b"ply\nformat binary_little_endian 1.0\n"):])
+    head2, _ = _ply_source(q)
+    schema, count, names2, _ = _parse_ply_header(head2, q)
+    assert count == big.shape[0] and names2 == names
