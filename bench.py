@@ -77,7 +77,7 @@ def parse():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--cpu-budget", type=float, default=12.0, help="seconds of sampled CPU render")
-    ap.add_argument("--streams", type=int, default=4,
+    ap.add_argument("--streams", type=int, default=8,
                     help="views in flight per GPU: one Rasterizer + stream each (frames of different "
                          "views overlap; each frame is still one CUDA graph)")
     return ap.parse_args()
