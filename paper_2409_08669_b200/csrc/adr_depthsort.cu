@@ -66,7 +66,10 @@ __global__ void __launch_bounds__(kSortBlock) k_ds_hist0(const uint32_t* __restr
 }
 
 // One onesweep pass (see the file comment).  vals_in == nullptr: identity.
-__global__ void __launch_bounds__(kSortBlock, 3)
+#ifndef ADR_DS_MINB
+#define ADR_DS_MINB 3
+#endif
+__global__ void __launch_bounds__(kSortBlock, ADR_DS_MINB)
 k_ds_pass(const uint32_t* __restrict__ keys_in, const uint32_t* __restrict__ vals_in, uint32_t* __restrict__ keys_out,
           uint32_t* __restrict__ vals_out, int64_t n, int pass, DepthPlan dp, DsBufs b,
           const uint2* __restrict__ gsrc, uint4* __restrict__ rinfo) {

@@ -350,7 +350,10 @@ __device__ __forceinline__ void preprocess_block(const T* __restrict__ centers, 
 // per SM (72 registers): with frames in flight, 64 registers (8 blocks) and
 // 80 (6 blocks) both measured 2-5% fewer frames/s (notes.md, experiment 8).
 template <typename T, int DEG, bool FUSED>
-__global__ void __launch_bounds__(kPreBlock, 7)
+#ifndef ADR_PRE_MINB
+#define ADR_PRE_MINB 7
+#endif
+__global__ void __launch_bounds__(kPreBlock, ADR_PRE_MINB)
 k_preprocess(const T* __restrict__ centers, const T* __restrict__ scales,
              const T* __restrict__ rotations, const T* __restrict__ opacities,
              const T* __restrict__ sh, int64_t n, adr_camera cam, int32_t mode,

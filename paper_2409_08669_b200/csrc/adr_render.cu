@@ -14,6 +14,10 @@
 #include "adr_kernels.cuh"
 #include "adr_scan.cuh"
 
+#ifndef ADR_RENDER_MINB
+#define ADR_RENDER_MINB 8
+#endif
+
 namespace adr {
 
 // Self-check instantiation (k_render<Src, true>, selected at run time by
@@ -34,7 +38,7 @@ constexpr int kBatch = 256;               // pairs staged per round
 
 // Record source for the fused frame: records by rank + per-pair rank list.
 struct RecSource {
-    static constexpr int kMinBlocks = 8;   // 64 registers (8 blocks/SM: +0.6% frames/s over 7, notes exp. 9)
+    static constexpr int kMinBlocks = ADR_RENDER_MINB;   // 8: 64 registers (8 blocks/SM: +0.6% frames/s over 7, notes exp. 9)
     const Record* rec;
     const uint32_t* idx;
     __device__ __forceinline__ Record load(int64_t j) const { return rec[idx[j]]; }

@@ -255,7 +255,10 @@ __global__ void __launch_bounds__(1024) k_st_scan1(uint32_t* __restrict__ H1, co
 // the lowest peer bumps the warp's running offset.  Items are staged in shared memory in bucket order (the block's
 // items of one supertile are contiguous in the output) and flushed as
 // coalesced runs.
-__global__ void __launch_bounds__(256, 4) k_st_scatter1(const uint4* __restrict__ rinfo, const int64_t* __restrict__ d_m,
+#ifndef ADR_SC1_MINB
+#define ADR_SC1_MINB 4
+#endif
+__global__ void __launch_bounds__(256, ADR_SC1_MINB) k_st_scatter1(const uint4* __restrict__ rinfo, const int64_t* __restrict__ d_m,
                                                      StGeom g, const uint32_t* __restrict__ H1, StCtl c,
                                                      StItems items, int64_t items_cap) {
     extern __shared__ __align__(16) unsigned char sc_raw[];
@@ -573,7 +576,10 @@ __global__ void __launch_bounds__(1024) k_st_scan2(uint32_t* __restrict__ U, StG
 //      (the warp's items on that tile, in rank order) and stage each item's
 //      {index, depth bits} at consecutive slots of the tile's run;
 //   D  (barrier) thread per slot: coalesced per-tile runs out; (barrier).
-__global__ void __launch_bounds__(256, 6) k_st_place(StItems items, StGeom g, StCtl c, int64_t items_cap,
+#ifndef ADR_PLACE_MINB
+#define ADR_PLACE_MINB 6
+#endif
+__global__ void __launch_bounds__(256, ADR_PLACE_MINB) k_st_place(StItems items, StGeom g, StCtl c, int64_t items_cap,
                                                   const uint32_t* __restrict__ C2, const uint32_t* __restrict__ U,
                                                   const int64_t* __restrict__ d_pc, uint32_t* __restrict__ gidx_out,
                                                   uint64_t* __restrict__ keys_out) {
