@@ -26,6 +26,7 @@ from __future__ import annotations
 import argparse
 import ctypes
 import json
+import math
 import os
 import statistics
 import subprocess
@@ -77,7 +78,7 @@ def parse():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--cpu-budget", type=float, default=12.0, help="seconds of sampled CPU render")
-    ap.add_argument("--streams", type=int, default=8,
+    ap.add_argument("--streams", type=int, default=4,
                     help="views in flight per GPU: one Rasterizer + stream each (frames of different "
                          "views overlap; each frame is still one CUDA graph)")
     return ap.parse_args()
@@ -391,10 +392,13 @@ def run_ours(args, cfg, rank, world, local):
     clocks.start()
     time.sleep(0.3)
     ms = timed(args.steps, gather=True)   # the headline: render + gather to rank 0
-    soak_end = time.perf_counter() + max(0.0, 1.5 - ms * 1e-3)
-    while time.perf_counter() < soak_end:   # keep the clock sampler under load >= 1.5 s
+    # keep the clock sampler under load >= 1.5 s; the step count derives from
+    # the max-reduced time, so every rank runs the same number of gathered
+    # steps (a wall-clock loop could leave one rank's frame sends unmatched)
+    n_soak = int(math.ceil(max(0.0, 1.5 - ms * 1e-3) / max(ms * 1e-3 / args.steps, 1e-6)))
+    for _ in range(n_soak):
         step(True)
-        torch.cuda.synchronize(dev)
+    torch.cuda.synchronize(dev)
     clk = clocks.stop()
     frames = views * args.steps
     value = frames / (ms * 1e-3)
@@ -430,7 +434,13 @@ def run_ours(args, cfg, rank, world, local):
 
     # e2e legs (per rank; aggregated over ranks)
     e2e = e2e_frame = e2e_res = e2e_rp = None
-    if not args.no_e2e and n_mine:
+    # the e2e legs hold barriers and reductions: every rank must agree to run them
+    run_e2e = not args.no_e2e and n_mine > 0
+    if dist:
+        t = torch.tensor([1.0 if run_e2e else 0.0], dtype=torch.float64, device=dev)
+        reduce_(t, op=dist.ReduceOp.MIN)
+        run_e2e = bool(t.item() > 0.5)
+    if run_e2e:
         src = [host.centers, host.scales, host.rotations, host.opacities, host.sh]
         dst = [ds.centers, ds.scales, ds.rotations, ds.opacities, ds.sh]
         h2d = host.nbytes()
