@@ -320,7 +320,7 @@ def run_ours(args, cfg, rank, world, local):
         pairs.append(res.stats.pair_count)
     rast.fit_capacity(max(pairs) if pairs else 0)
     v0 = mine[0] if mine else 0
-    for _ in range(3):
+    for _ in range(10):   # per-stage CUDA-event durations (the roofline's denominators)
         res = rast.render(ds, cams[v0], mode=cfg["mode"])
         stage_ms.append({k: v * 1e3 for k, v in res.stats.stage_seconds().items()})
     first = rast.render(ds, cams[v0], mode=cfg["mode"])
@@ -591,7 +591,10 @@ def run_ours(args, cfg, rank, world, local):
                          "bytes_rule": "SURVEY.md §8(d): N(44+12K) read + 52N write",
                          "impl_bytes_per_launch": pre_impl_bytes,
                          "impl_frac": pre_impl_bytes / (med["preprocess"] * 1e-3) / 1e9 / hbm,
-                         "peak_kind": peak_kind},
+                         "peak_kind": peak_kind,
+                         "duration_ms": med["preprocess"],
+                         "duration_source": "median of CUDA events around the stage in 10 frames of the "
+                                            "bench view rendered one at a time (no other frame in flight)"},
             "binning_roofline": {"bound": "hbm", "kernels": "depth sort + supertile items + pair placement",
                                  "bytes_per_frame": bin_bytes,
                                  "bytes_rule": "SURVEY.md §8(d): N·16 dup read + P·12 pair write + P·24 one ideal sort pass",
