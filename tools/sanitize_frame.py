@@ -1,7 +1,9 @@
 """One small fused frame + the stage API + the GPU reference renderer, for
 compute-sanitizer (memcheck / racecheck / synccheck / initcheck):
 
-    compute-sanitizer --tool memcheck python tools/sanitize_frame.py
+    compute-sanitizer --tool memcheck python tools/sanitize_frame.py [N]
+
+With N, one N-Gaussian 640x360 frame instead (multi-block sort / binning).
 """
 import sys
 from pathlib import Path
@@ -16,6 +18,17 @@ import paper_2409_08669_b200 as ab  # noqa: E402
 
 def main():
     spec = ab.SyntheticSpec(extent=1.0, scale_range=(0.004, 0.05), anisotropy_range=(1, 5), opacity_range=(0.01, 0.95))
+    if len(sys.argv) > 1:   # a multi-block frame: depth-sort look-back chains, many supertile chunks
+        n = int(sys.argv[1])
+        a = ab.synthetic_arrays(6, n, spec, sh_degree=3, float32=True)
+        ds = ab.DeviceScene.from_arrays(a, 3, "cuda", torch.float32)
+        cam = ab.Camera.from_lookat((0.3, -0.2, -2.6), (0, 0, 0), width=640, height=360, background=(0.1, 0.2, 0.3))
+        res = ab.run_pipeline(ds, cam, mode="aabb")
+        ref_img, _ = ab.render_reference(ds, cam)
+        torch.cuda.synchronize()
+        assert torch.equal(ref_img.pixels.view(torch.int32), res.image.pixels.view(torch.int32))
+        print("sanitize frame OK", n, "Gaussians", res.stats.pair_count, "pairs")
+        return
     a = ab.synthetic_arrays(5, 4000, spec, sh_degree=3, float32=True)
     ds = ab.DeviceScene.from_arrays(a, 3, "cuda", torch.float32)
     cam = ab.Camera.from_lookat((0.3, -0.2, -2.6), (0, 0, 0), width=200, height=136, background=(0.1, 0.2, 0.3))
