@@ -537,6 +537,8 @@ def run_ours(args, cfg, rank, world, local):
             ems, fms, rms, rp_s = (float(v) for v in t.tolist())
         e2e = {"value": views * k_e2e / (ems * 1e-3), "unit": "frames/s",
                "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h_frame * n_mine,
+               # per rank: the scene upload is the bound (PCIe Gen5 x16 moves ~55 GB/s)
+               "h2d_gbs_per_rank": h2d * k_e2e / (ems * 1e-3) / 1e9,
                "path": "per step (as in value: this rank's views of the batch): the scene H2D from pinned "
                        "host memory, every view through the C-ABI frame call (Rasterizer.launch, no graph), "
                        "each image + load map D2H to pinned host memory; double-buffered device scene (step "
