@@ -182,18 +182,40 @@ k_ds_pass(const uint32_t* __restrict__ keys_in, const uint32_t* __restrict__ val
     }
     __syncthreads();
     const int live = (int)((n - base) < kDsTile ? (n - base) : kDsTile);
+    if (last) {
+        // the tile-rect gathers of ADR_DS_GATHER items in flight per thread
+        // before their rank records are written
+#ifndef ADR_DS_GATHER
+#define ADR_DS_GATHER 4
+#endif
+        constexpr int U = ADR_DS_GATHER;
+        for (int i0 = threadIdx.x; i0 < live; i0 += U * kSortBlock) {
+            uint32_t key[U], val[U];
+            uint2 r[U];
+#pragma unroll
+            for (int u = 0; u < U; ++u) {
+                const int i = i0 + u * kSortBlock;
+                key[u] = i < live ? skeys[i] : 0u;
+                val[u] = i < live ? svals[i] : 0u;
+                r[u] = i < live ? __ldg(gsrc + val[u]) : make_uint2(0u, 0u);
+            }
+#pragma unroll
+            for (int u = 0; u < U; ++u) {
+                const int i = i0 + u * kSortBlock;
+                if (i < live) {
+                    const int64_t g = goff[(key[u] >> bit) & 0xffu] + i;
+                    const uint32_t kk = fits ? (key[u] == 0xffffffu ? 0xffffffffu : key[u] + kmin) : key[u];
+                    rinfo[g] = make_uint4(val[u], kk, r[u].x, r[u].y);
+                }
+            }
+        }
+        return;
+    }
     for (int i = threadIdx.x; i < live; i += kSortBlock) {
         const uint32_t key = skeys[i];
-        const uint32_t val = svals[i];
         const int64_t g = goff[(key >> bit) & 0xffu] + i;
-        if (last) {
-            const uint2 r = __ldg(gsrc + val);
-            const uint32_t kk = fits ? (key == 0xffffffu ? 0xffffffffu : key + kmin) : key;
-            rinfo[g] = make_uint4(val, kk, r.x, r.y);
-        } else {
-            keys_out[g] = key;
-            vals_out[g] = val;
-        }
+        keys_out[g] = key;
+        vals_out[g] = svals[i];
     }
 }
 
