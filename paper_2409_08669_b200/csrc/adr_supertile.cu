@@ -52,8 +52,14 @@ namespace {
 constexpr int kStSide = 8;            // supertile side in tiles
 constexpr int kL1Ranks = 256;         // ranks per L1 warp chunk
 constexpr int kL1Block = 8 * kL1Ranks; // ranks per L1 block (h1b column entry, scatter block)
-constexpr int kL1Cap = 4096;          // items staged per L1 scatter window
-constexpr int kXList = 64;            // per-warp expanded-item list of the L1 scatter (one round segment)
+#ifndef ADR_L1CAP
+#define ADR_L1CAP 4096
+#endif
+#ifndef ADR_XLIST
+#define ADR_XLIST 64
+#endif
+constexpr int kL1Cap = ADR_L1CAP;     // items staged per L1 scatter window
+constexpr int kXList = ADR_XLIST;     // per-warp expanded-item list of the L1 scatter (one round segment)
 constexpr int kChunk = 256;           // items per L2 chunk (= one 256-thread block)
 constexpr int kStageCap = 3072;       // pairs staged per placement window
 
@@ -442,7 +448,10 @@ __device__ __forceinline__ int64_t live_chunks(const StCtl& c, int S, int64_t it
 // (persistent): for each chunk, 8 rounds of cover popcounts per local tile;
 // C2[chunk * 64 + l] = pairs of tile l in the unit's earlier chunks, U[unit *
 // 64 + l] = the unit's total.
-__global__ void __launch_bounds__(256) k_st_count2(StItems items, StGeom g, StCtl c, int64_t items_cap,
+#ifndef ADR_C2_MINB
+#define ADR_C2_MINB 1
+#endif
+__global__ void __launch_bounds__(256, ADR_C2_MINB) k_st_count2(StItems items, StGeom g, StCtl c, int64_t items_cap,
                                                    uint32_t* __restrict__ C2, uint32_t* __restrict__ U) {
     const int lane = threadIdx.x & 31;
     const int64_t n2 = live_chunks(c, g.S, items_cap);
