@@ -27,7 +27,10 @@ namespace adr {
 namespace {
 
 constexpr int kDsR = 256;                         // 8-bit digits
-constexpr int kDsIpt = 16;                        // keys per thread
+#ifndef ADR_DS_IPT
+#define ADR_DS_IPT 16
+#endif
+constexpr int kDsIpt = ADR_DS_IPT;                // keys per thread
 constexpr int kDsTile = kSortBlock * kDsIpt;      // 4096 keys per block
 
 struct DsBufs {
