@@ -34,7 +34,10 @@ __device__ unsigned long long g_render_prof[8];
 namespace {
 
 constexpr int kRenderThreads = 128;       // 2 pixels per thread
-constexpr int kBatch = 256;               // pairs staged per round
+#ifndef ADR_RBATCH
+#define ADR_RBATCH 256
+#endif
+constexpr int kBatch = ADR_RBATCH;        // pairs staged per round
 
 // Record source for the fused frame: records by rank + per-pair rank list.
 struct RecSource {
