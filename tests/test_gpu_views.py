@@ -86,3 +86,27 @@ def test_render_views_sharded_two_processes():
         ls = res.load_stats
         assert int(st[i, 0]) == res.stats.pair_count and int(st[i, 1]) == res.stats.culled_gaussians
         assert int(st[i, 4]) == ls.min and int(st[i, 5]) == ls.max
+
+
+def test_bench_multi_rank_path_completes():
+    """bench.py's multi-rank path (torchrun, two ranks over gloo on cuda:0):
+    every loop around a frame transfer or collective runs a rank-agreed
+    number of steps, so the run ends (a wall-clock soak loop once left one
+    rank's sends unmatched), and rank 0 prints one JSON line with the
+    gathered frames counted over both ranks."""
+    import json
+    import subprocess
+
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        port = s.getsockname()[1]
+    env = dict(os.environ, ADR_BENCH_BACKEND="gloo")
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", "2",
+           "--master-addr", "127.0.0.1", "--master-port", str(port), str(ROOT / "bench.py"), "--gpus", "2",
+           "--config", "config1", "--steps", "3", "--warmup", "3", "--no-cpu-baseline"]
+    out = subprocess.run(cmd, cwd=ROOT, env=env, capture_output=True, text=True, timeout=600)
+    assert out.returncode == 0, out.stderr[-2000:]
+    lines = [ln for ln in out.stdout.splitlines() if ln.startswith("{")]
+    assert len(lines) == 1
+    d = json.loads(lines[0])
+    assert d["n_gpus"] == 2 and d["value"] > 0 and d["e2e"]["value"] > 0
