@@ -81,6 +81,9 @@ def parse():
     ap.add_argument("--streams", type=int, default=4,
                     help="views in flight per GPU: one Rasterizer + stream each (frames of different "
                          "views overlap; each frame is still one CUDA graph)")
+    ap.add_argument("--batch-views", type=int, default=8,
+                    help="views per stage-1 launch (adr_preprocess_views: the scene is read once for the "
+                         "batch); 1 = one adr_render_frame graph per view")
     return ap.parse_args()
 
 
@@ -336,6 +339,44 @@ def run_ours(args, cfg, rank, world, local):
                                     timing=False) for _ in range(n_fly - 1)]
     streams = [torch.cuda.Stream(dev) for _ in range(n_fly)]
     graphs = [rasts[j % n_fly].capture(ds, cams[v], mode=cfg["mode"]) for j, v in enumerate(mine)]
+    # batched stage 1: groups of G consecutive views share one preprocess_views
+    # launch (one scene read); two slot sets alternate so group g+1's stage 1
+    # overlaps group g's binning + render
+    G = max(1, min(args.batch_views, ab.MAX_BATCH_VIEWS, max(n_mine, 1)))
+    groups = [list(range(i, min(i + G, n_mine))) for i in range(0, n_mine, G)] if G > 1 else []
+    n_sets = min(2, len(groups))
+    slots, pre_graphs, post_graphs, pre_streams = [], [], [], []
+    if groups:
+        slots = rasts[:G * n_sets] + [ab.Rasterizer(cfg["w"], cfg["h"], cfg["n"], device=dev, pair_capacity=rast.cap,
+                                                    timing=False) for _ in range(G * n_sets - len(rasts))]
+        pre_streams = [torch.cuda.Stream(dev) for _ in range(n_sets)]
+
+        def capture(fn):
+            g = torch.cuda.CUDAGraph()
+            cs = torch.cuda.Stream(dev)
+            cs.wait_stream(torch.cuda.current_stream(dev))
+            torch.cuda.synchronize(dev)
+            with torch.cuda.graph(g, stream=cs):
+                fn(cs)
+            torch.cuda.synchronize(dev)
+            return g
+
+        post_graphs = [None] * n_mine
+        for gi, grp in enumerate(groups):
+            sl = [slots[(gi % n_sets) * G + q] for q in range(len(grp))]
+            gc = [cams[mine[j]] for j in grp]
+            before_b = L.adr_kernel_launches()
+            ab.render_views_batched(ds, gc, sl, mode=cfg["mode"])   # eager run before capture
+            torch.cuda.synchronize(dev)
+            if gi == 0:
+                launches_per_frame = (L.adr_kernel_launches() - before_b) / len(grp)
+            for r_ in sl:
+                assert not r_.truncated()
+            pre_graphs.append(capture(lambda cs, gc=gc, sl=sl: ab.preprocess_views(ds, gc, sl, mode=cfg["mode"],
+                                                                                   stream=cs)))
+            for q, j in enumerate(grp):
+                post_graphs[j] = capture(lambda cs, r_=sl[q], c_=gc[q]: r_.launch_post(ds, c_, mode=cfg["mode"],
+                                                                                       stream=cs))
     fg = FrameGather(views, cfg["h"], cfg["w"], dev) if world > 1 else None
     zero = torch.zeros(1, dtype=torch.int64, device=dev)
     setup_s = time.perf_counter() - t_setup
@@ -364,6 +405,64 @@ def run_ours(args, cfg, rank, world, local):
             stream.wait_event(ev)
         if fg is not None and gather:
             fg.finish()
+
+    bpre_ms = None
+    if groups:   # the batched stage-1 launch alone (its roofline denominator)
+        ts = []
+        for _ in range(7):
+            q0, q1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            q0.record(stream)
+            pre_graphs[0].replay()
+            q1.record(stream)
+            torch.cuda.synchronize(dev)
+            ts.append(q0.elapsed_time(q1))
+        bpre_ms = statistics.median(ts[2:])
+
+    def step_batched(gather: bool):
+        """One batch through batched stage 1: per group of G views one
+        preprocess_views graph on its slot set's stream, then each view's
+        stages 2-6 graph on the in-flight streams (gathered like `step`)."""
+        ev0 = torch.cuda.Event()
+        ev0.record(stream)
+        for st in streams + pre_streams:
+            st.wait_event(ev0)
+        if fg is not None and gather:
+            fg.begin()
+        pending = [[] for _ in range(n_sets)]
+        for gi, grp in enumerate(groups):
+            ss = gi % n_sets
+            ps = pre_streams[ss]
+            for e in pending[ss]:
+                ps.wait_event(e)
+            with torch.cuda.stream(ps):
+                pre_graphs[gi].replay()
+            pe = torch.cuda.Event()
+            pe.record(ps)
+            used = []
+            for q, j in enumerate(grp):
+                k = j % n_fly
+                streams[k].wait_event(pe)
+                with torch.cuda.stream(streams[k]):
+                    post_graphs[j].replay()
+                    if fg is not None and gather:
+                        r = slots[ss * G + q]
+                        fg.send(mine[j], r.pixels, r.load, torch.cat([r.counters[0:2], r.stats[0:3], zero]))
+                if k not in used:
+                    used.append(k)
+            pending[ss] = []
+            for k in used:
+                e = torch.cuda.Event()
+                e.record(streams[k])
+                pending[ss].append(e)
+        for st in streams + pre_streams:
+            ev = torch.cuda.Event()
+            ev.record(st)
+            stream.wait_event(ev)
+        if fg is not None and gather:
+            fg.finish()
+
+    if groups:
+        step = step_batched  # noqa: F811
 
     def timed(k_steps: int, gather: bool) -> float:
         torch.cuda.synchronize(dev)
@@ -566,7 +665,10 @@ def run_ours(args, cfg, rank, world, local):
     if rank == 0:
         cfgd = config_dict(cfg, args, views, world, p_mean, scaling)
         cfgd.update({"step": f"{views} views rendered (view-sharded) + gathered to rank 0",
-                     "frame": "CUDA graph per view, no host sync", "views_in_flight": n_fly})
+                     "frame": (f"stage 1 of {G} views per launch (preprocess_views graph, scene read once per "
+                               f"group), stages 2-6 a CUDA graph per view, no host sync" if groups else
+                               "CUDA graph per view, no host sync"),
+                     "views_in_flight": n_fly, "batch_views": G if groups else 1})
         line = {
             "metric": METRIC, "value": value, "unit": "frames/s", "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_per_step,
@@ -597,6 +699,15 @@ def run_ours(args, cfg, rank, world, local):
                          "duration_ms": med["preprocess"],
                          "duration_source": "median of CUDA events around the stage in 10 frames of the "
                                             "bench view rendered one at a time (no other frame in flight)"},
+            "batch_preprocess": None if bpre_ms is None else {
+                "kernel": "k_preprocess_views", "views_per_launch": len(groups[0]), "ms": bpre_ms,
+                "ms_per_view": bpre_ms / len(groups[0]),
+                "bytes_per_launch": n * (44 + 12 * k_sh) + len(groups[0]) * n * 52,
+                "bytes_rule": "SURVEY.md §8(d) with the scene read once per launch: N(44+12K) + views·52N",
+                "achieved": (n * (44 + 12 * k_sh) + len(groups[0]) * n * 52) / (bpre_ms * 1e-3) / 1e9,
+                "frac": (n * (44 + 12 * k_sh) + len(groups[0]) * n * 52) / (bpre_ms * 1e-3) / 1e9 / hbm,
+                "per_view_equivalent_gbs": pre_bytes * len(groups[0]) / (bpre_ms * 1e-3) / 1e9,
+                "duration_source": "median of CUDA events around the group-0 stage-1 graph replayed alone"},
             "binning_roofline": {"bound": "hbm", "kernels": "depth sort + supertile items + pair placement",
                                  "bytes_per_frame": bin_bytes,
                                  "bytes_rule": "SURVEY.md §8(d): N·16 dup read + P·12 pair write + P·24 one ideal sort pass",
@@ -614,7 +725,7 @@ def run_ours(args, cfg, rank, world, local):
             "frame_roofline": {"bytes_per_frame": falg, "achieved_gbs": falg * value / world / 1e9,
                                "frac": falg * value / world / 1e9 / hbm,
                                "bytes_rule": "SURVEY.md §8(d): N(112+12K) + 84P + 16HW"},
-            "clocks": clk, "gpu_launches": launches_per_frame * frames,
+            "clocks": clk, "gpu_launches": int(round(launches_per_frame * frames)),
             "launches_per_frame": launches_per_frame, "setup_s": setup_s,
         }
         if e2e:

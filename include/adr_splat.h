@@ -27,7 +27,7 @@
 extern "C" {
 #endif
 
-#define ADR_ABI_VERSION 2
+#define ADR_ABI_VERSION 3
 
 typedef enum {
     ADR_OK = 0,
@@ -281,6 +281,27 @@ size_t adr_frame_record_offset(int64_t n, int32_t width, int32_t height, int64_t
 int32_t adr_render_frame(const adr_scene* scene, const adr_camera* cam, int32_t mode,
                          double alpha_low, double dilation, double term_threshold,
                          const adr_frame_buffers* buf, void* stream);
+
+/* Batched frames of one scene (no reference counterpart to replace: the
+ * reference renders one view per run_pipeline call, sb/pipeline.py:85-124;
+ * this is that call split at its stage-1 boundary, sb/pipeline.py:98).
+ *
+ * adr_preprocess_views: stage 1 of n_views (1..8) frames in ONE launch.  Each
+ * Gaussian's row and SH coefficients are read once and its view-independent
+ * terms (cov3d, ln(sigma / alpha_low)) evaluated once; every view's
+ * Projection, render record, tile rect and depth key are written into bufs[v]
+ * (an array of n_views frame buffers, each its own scratch and counters),
+ * bit-identical to adr_render_frame's stage 1 for (scene, cams[v]).
+ * adr_render_frame_post: stages 2-6 of a frame whose stage 1 ran through
+ * adr_preprocess_views (same scene, camera, mode, alpha_low; enqueue it after
+ * that launch, e.g. on another stream behind an event).  Together they give
+ * exactly adr_render_frame's outputs.  Events [0] and [1] are not recorded. */
+int32_t adr_preprocess_views(const adr_scene* scene, const adr_camera* cams, int32_t n_views,
+                             int32_t mode, double alpha_low, double dilation,
+                             const adr_frame_buffers* bufs, void* stream);
+int32_t adr_render_frame_post(const adr_scene* scene, const adr_camera* cam, int32_t mode,
+                              double alpha_low, double dilation, double term_threshold,
+                              const adr_frame_buffers* buf, void* stream);
 
 #ifdef __cplusplus
 }

@@ -15,7 +15,8 @@ from .footprint import (CullExtent, EllipseCoefficients, ProjectedGaussian, aabb
 from .metrics import (DEFAULT_WEIGHTS, PSNR_IDENTICAL_SENTINEL, BalanceStepResult, LoadStats,
                       LossWeights, l1_loss, load_loss, psnr, replace_opacity, ssim, toy_balance_step,
                       total_loss)
-from .pipeline import STAGE_NAMES, PipelineResult, Rasterizer, RenderStats, run_pipeline
+from .pipeline import (MAX_BATCH_VIEWS, STAGE_NAMES, PipelineResult, Rasterizer, RenderStats,
+                       preprocess_views, render_views_batched, run_pipeline)
 from .projection import (ALPHA_LOW, BASE_RADIUS_MULTIPLIER, COV_DILATION, FOV_CLAMP_FACTOR,
                          CullingMode, Projection, preprocess)
 from .refrender import render_reference
@@ -45,5 +46,5 @@ __all__ = [
     "composite_pixels", "eigen_extents", "ellipse_coefficients", "evaluate_sh", "project_gaussian",
     "quaternion_to_rotation", "radius_adaptive", "radius_baseline", "replace_opacity", "ssim", "toy_balance_step", "total_loss", "duplicate_with_keys", "generate_synthetic",
     "identify_tile_ranges", "inclusive_sum", "load_loss", "preprocess", "psnr", "render",
-    "run_pipeline", "sort_pairs", "synthetic_arrays", "tiles_touched", "touched_counts",
+    "run_pipeline", "sort_pairs", "MAX_BATCH_VIEWS", "preprocess_views", "render_views_batched", "synthetic_arrays", "tiles_touched", "touched_counts",
 ]

@@ -33,7 +33,7 @@ EXPORTED = (
     "adr_duplicate_with_keys", "adr_sort_pairs_scratch_bytes", "adr_sort_pairs",
     "adr_identify_tile_ranges", "adr_render", "adr_exp_np_f32", "adr_selftest_exp", "adr_exp_checksum", "adr_exp64_checksum", "adr_render_selfcheck",
     "adr_ply_status_reset", "adr_ply_activate",
-    "adr_frame_scratch_bytes", "adr_frame_record_offset", "adr_render_frame", "adr_image_loss_scratch_bytes", "adr_image_losses",
+    "adr_frame_scratch_bytes", "adr_frame_record_offset", "adr_render_frame", "adr_preprocess_views", "adr_render_frame_post", "adr_image_loss_scratch_bytes", "adr_image_losses",
     "adr_render_reference_scratch_bytes", "adr_render_reference",
 )
 
@@ -124,6 +124,10 @@ def lib() -> ctypes.CDLL:
             "adr_frame_record_offset": (sz, [i64, i32, i32, i64]),
             "adr_render_frame": (i32, [P(Scene_t), P(Camera_t), i32, dbl, dbl, dbl,
                                        P(FrameBuffers_t), vp]),
+            "adr_preprocess_views": (i32, [P(Scene_t), P(Camera_t), i32, i32, dbl, dbl,
+                                           P(FrameBuffers_t), vp]),
+            "adr_render_frame_post": (i32, [P(Scene_t), P(Camera_t), i32, dbl, dbl, dbl,
+                                            P(FrameBuffers_t), vp]),
             "adr_image_loss_scratch_bytes": (sz, [i32, i32]),
             "adr_image_losses": (i32, [vp, vp, i32, i32, P(dbl), dbl, dbl, vp, vp, sz, vp]),
             "adr_render_reference_scratch_bytes": (sz, [i64]),
@@ -133,7 +137,7 @@ def lib() -> ctypes.CDLL:
             fn = getattr(L, name)
             fn.restype = res
             fn.argtypes = args
-        if L.adr_abi_version() != 2:
+        if L.adr_abi_version() != 3:
             raise RuntimeError("libadrsplat ABI mismatch")
         _lib = L
     return _lib

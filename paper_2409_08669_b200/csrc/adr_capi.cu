@@ -64,6 +64,121 @@ size_t frame_bytes(int64_t n, int32_t tx, int32_t ty, int64_t cap, FrameLayout* 
 
 }  // namespace adr
 
+
+namespace adr {
+namespace {
+
+// Per-frame layout and the fused stage-1 extras of one frame's buffers.
+struct FrameSetup {
+    FrameLayout L;
+    FusedPre fp;
+    cudaEvent_t ev[7] = {};
+    int32_t tx = 0, ty = 0;
+    int64_t n_tiles = 0;
+    double alpha_low = 0.0;
+};
+
+int32_t frame_setup(const adr_scene* scene, const adr_camera* cam, double alpha_low, const adr_frame_buffers* buf,
+                    FrameSetup* f) {
+    if (!scene || !cam || !buf) return fail(ADR_ERR_VALUE, "null argument");
+    if (cam->width < 1 || cam->height < 1) return fail(ADR_ERR_VALUE, "grid dimensions must be positive");
+    f->tx = tiles_of(cam->width);
+    f->ty = tiles_of(cam->height);
+    f->n_tiles = (int64_t)f->tx * f->ty;
+    if (f->n_tiles >= (int64_t(1) << 32)) return fail(ADR_ERR_CAPACITY, "tile count does not fit the 32-bit key field");
+    const size_t need = frame_bytes(scene->n, f->tx, f->ty, buf->pair_capacity, &f->L, buf->d_scratch,
+                                    buf->scratch_bytes);
+    if (need > buf->scratch_bytes) return fail(ADR_ERR_VALUE, "render_frame: scratch too small");
+    if (buf->events)
+        for (int i = 0; i < 7; ++i) f->ev[i] = reinterpret_cast<cudaEvent_t>(buf->events[i]);
+    f->alpha_low = alpha_low;
+    FusedPre& fp = f->fp;
+    fp.rec = f->L.rec;
+    fp.gpack = f->L.gpack;
+    fp.dkey = f->L.dkey;
+    fp.d_m = buf->d_counters + 2;
+    fp.culled = reinterpret_cast<unsigned long long*>(buf->d_counters + 1);
+    fp.nan_colors = reinterpret_cast<unsigned long long*>(buf->d_counters + 4);
+    fp.ambiguous = reinterpret_cast<unsigned long long*>(buf->d_counters + 5);
+    fp.tiles_x = f->tx;
+    fp.tiles_y = f->ty;
+    fp.kminmax = supertile_path(f->n_tiles, f->tx, f->ty) ? f->L.kminmax : nullptr;
+    fp.rec_only = buf->projection_in_record != 0;
+    fp.ln_a32_a64 = std::log((double)(float)alpha_low / alpha_low);
+    fp.plan_mm = fp.kminmax ? f->L.plan_mm : nullptr;
+    return ADR_OK;
+}
+
+// Stages 2-6 of a frame whose stage 1 (fused) has run on `st` or before it.
+int32_t frame_post(const adr_scene& scene, const adr_camera& cam, double term_threshold,
+                   const adr_frame_buffers* buf, const FrameSetup& f, cudaStream_t st) {
+    const int64_t n = scene.n;
+    const FrameLayout& L = f.L;
+    const cudaEvent_t* ev = f.ev;
+    int32_t rc = ADR_OK;
+    if (n > 0) {
+        FrameBinning fb;
+        fb.proj = buf->proj;
+        fb.n = n;
+        fb.cap = buf->pair_capacity;
+        fb.n_tiles = f.n_tiles;
+        fb.tiles_x = f.tx;
+        fb.tiles_y = f.ty;
+        fb.dkey = L.dkey;
+        fb.order = L.order;
+        fb.gpack = L.gpack;
+        fb.kminmax = f.fp.kminmax;
+        fb.plan_mm = f.fp.plan_mm;
+        fb.ranges = buf->d_ranges;
+        fb.keys = buf->d_keys;
+        fb.gidx = buf->d_gidx;
+        fb.counters = buf->d_counters;
+        fb.stats = buf->d_hist ? nullptr : buf->d_stats;   // with a histogram the init kernel runs
+        fb.scratch = L.binning;
+        fb.scratch_bytes = L.binning_bytes;
+        fb.ev_after_scan = ev[2];
+        fb.ev_after_dup = ev[3];
+        fb.ev_after_sort = ev[4];
+        fb.ev_after_ranges = ev[5];
+        rc = frame_binning(fb, st);
+        if (rc) return rc;
+    } else {
+        ADR_CUDA_TRY(cudaMemsetAsync(buf->d_ranges, 0, sizeof(int64_t) * 2 * f.n_tiles, st));
+        for (int i = 2; i <= 5; ++i)
+            if (ev[i]) ADR_CUDA_TRY(cudaEventRecord(ev[i], st));
+    }
+
+    if (n <= 0 || buf->d_hist) {
+        rc = launch_init_stats(buf->d_stats, buf->d_hist, buf->hist_bins, st);
+        if (rc) return rc;
+    }
+    RenderArgs ra;
+    ra.rec = L.rec;
+    ra.idx = reinterpret_cast<const uint32_t*>(buf->d_gidx);
+    ra.ranges = buf->d_ranges;
+    ra.order = nullptr;  // longest-span-first order measured no gain (profiles/r01_notes.md)
+    ra.width = cam.width;
+    ra.height = cam.height;
+    ra.tiles_x = f.tx;
+    ra.tiles_y = f.ty;
+    for (int i = 0; i < 3; ++i) ra.bg[i] = cam.background[i];
+    ra.alpha_low = (float)f.alpha_low;
+    ra.term = (float)term_threshold;
+    ra.pixels = buf->d_pixels;
+    ra.load = buf->d_load;
+    ra.stats = buf->d_stats;
+    ra.hist = buf->d_hist;
+    ra.hist_bins = buf->hist_bins;
+    ra.nan_flag = buf->d_counters + 4;
+    rc = launch_render(ra, st);
+    if (rc) return rc;
+    if (ev[6]) ADR_CUDA_TRY(cudaEventRecord(ev[6], st));
+    return ADR_OK;
+}
+
+}  // namespace
+}  // namespace adr
+
 using namespace adr;
 
 extern "C" {
@@ -145,98 +260,48 @@ size_t adr_frame_scratch_bytes(int64_t n, int32_t width, int32_t height, int64_t
 
 int32_t adr_render_frame(const adr_scene* scene, const adr_camera* cam, int32_t mode, double alpha_low,
                          double dilation, double term_threshold, const adr_frame_buffers* buf, void* stream) {
-    if (!scene || !cam || !buf) return fail(ADR_ERR_VALUE, "null argument");
-    if (cam->width < 1 || cam->height < 1) return fail(ADR_ERR_VALUE, "grid dimensions must be positive");
+    FrameSetup f;
+    int32_t rc = frame_setup(scene, cam, alpha_low, buf, &f);
+    if (rc) return rc;
     cudaStream_t st = as_stream(stream);
-    const int32_t tx = tiles_of(cam->width), ty = tiles_of(cam->height);
-    const int64_t n_tiles = (int64_t)tx * ty;
-    if (n_tiles >= (int64_t(1) << 32)) return fail(ADR_ERR_CAPACITY, "tile count does not fit the 32-bit key field");
-    const int64_t n = scene->n;
-    FrameLayout L;
-    const size_t need = frame_bytes(n, tx, ty, buf->pair_capacity, &L, buf->d_scratch, buf->scratch_bytes);
-    if (need > buf->scratch_bytes) return fail(ADR_ERR_VALUE, "render_frame: scratch too small");
-    cudaEvent_t ev[7] = {};
-    if (buf->events)
-        for (int i = 0; i < 7; ++i) ev[i] = reinterpret_cast<cudaEvent_t>(buf->events[i]);
-
     ADR_CUDA_TRY(cudaMemsetAsync(buf->d_counters, 0, 8 * sizeof(int64_t), st));
-    if (ev[0]) ADR_CUDA_TRY(cudaEventRecord(ev[0], st));
-    FusedPre fp;
-    fp.rec = L.rec;
-    fp.gpack = L.gpack;
-    fp.dkey = L.dkey;
-    fp.d_m = buf->d_counters + 2;
-    fp.culled = reinterpret_cast<unsigned long long*>(buf->d_counters + 1);
-    fp.nan_colors = reinterpret_cast<unsigned long long*>(buf->d_counters + 4);
-    fp.ambiguous = reinterpret_cast<unsigned long long*>(buf->d_counters + 5);
-    fp.tiles_x = tx;
-    fp.tiles_y = ty;
-    fp.kminmax = supertile_path(n_tiles, tx, ty) ? L.kminmax : nullptr;
-    fp.rec_only = buf->projection_in_record != 0;
-    fp.ln_a32_a64 = std::log((double)(float)alpha_low / alpha_low);
-    fp.plan_mm = fp.kminmax ? L.plan_mm : nullptr;
-    int32_t rc = launch_preprocess(*scene, *cam, mode, alpha_low, dilation, buf->proj, &fp, st);
+    if (f.ev[0]) ADR_CUDA_TRY(cudaEventRecord(f.ev[0], st));
+    rc = launch_preprocess(*scene, *cam, mode, alpha_low, dilation, buf->proj, &f.fp, st);
     if (rc) return rc;
-    if (ev[1]) ADR_CUDA_TRY(cudaEventRecord(ev[1], st));
+    if (f.ev[1]) ADR_CUDA_TRY(cudaEventRecord(f.ev[1], st));
+    return frame_post(*scene, *cam, term_threshold, buf, f, st);
+}
 
-    if (n > 0) {
-        FrameBinning fb;
-        fb.proj = buf->proj;
-        fb.n = n;
-        fb.cap = buf->pair_capacity;
-        fb.n_tiles = n_tiles;
-        fb.tiles_x = tx;
-        fb.tiles_y = ty;
-        fb.dkey = L.dkey;
-        fb.order = L.order;
-        fb.gpack = L.gpack;
-        fb.kminmax = fp.kminmax;
-        fb.plan_mm = fp.plan_mm;
-        fb.ranges = buf->d_ranges;
-        fb.keys = buf->d_keys;
-        fb.gidx = buf->d_gidx;
-        fb.counters = buf->d_counters;
-        fb.stats = buf->d_hist ? nullptr : buf->d_stats;   // with a histogram the init kernel runs
-        fb.scratch = L.binning;
-        fb.scratch_bytes = L.binning_bytes;
-        fb.ev_after_scan = ev[2];
-        fb.ev_after_dup = ev[3];
-        fb.ev_after_sort = ev[4];
-        fb.ev_after_ranges = ev[5];
-        rc = frame_binning(fb, st);
+int32_t adr_preprocess_views(const adr_scene* scene, const adr_camera* cams, int32_t n_views, int32_t mode,
+                             double alpha_low, double dilation, const adr_frame_buffers* bufs, void* stream) {
+    if (!scene || !cams || !bufs) return fail(ADR_ERR_VALUE, "null argument");
+    if (n_views < 1 || n_views > kMaxBatchViews) return fail(ADR_ERR_VALUE, "n_views must lie in 1..8");
+    cudaStream_t st = as_stream(stream);
+    PreViews pv;
+    pv.nv = n_views;
+    for (int v = 0; v < n_views; ++v) {
+        FrameSetup f;
+        int32_t rc = frame_setup(scene, &cams[v], alpha_low, &bufs[v], &f);
         if (rc) return rc;
-    } else {
-        ADR_CUDA_TRY(cudaMemsetAsync(buf->d_ranges, 0, sizeof(int64_t) * 2 * n_tiles, st));
-        for (int i = 2; i <= 5; ++i)
-            if (ev[i]) ADR_CUDA_TRY(cudaEventRecord(ev[i], st));
+        for (int u = 0; u < v; ++u)
+            if (bufs[u].d_scratch == bufs[v].d_scratch || bufs[u].d_counters == bufs[v].d_counters)
+                return fail(ADR_ERR_VALUE, "preprocess_views: every view needs its own frame buffers");
+        ADR_CUDA_TRY(cudaMemsetAsync(bufs[v].d_counters, 0, 8 * sizeof(int64_t), st));
+        pv.cam[v] = cams[v];
+        pv.out[v] = bufs[v].proj;
+        pv.fused[v] = f.fp;
     }
+    return launch_preprocess_views(*scene, pv, mode, alpha_low, dilation, st);
+}
 
-    if (n <= 0 || buf->d_hist) {
-        rc = launch_init_stats(buf->d_stats, buf->d_hist, buf->hist_bins, st);
-        if (rc) return rc;
-    }
-    RenderArgs ra;
-    ra.rec = L.rec;
-    ra.idx = reinterpret_cast<const uint32_t*>(buf->d_gidx);
-    ra.ranges = buf->d_ranges;
-    ra.order = nullptr;  // longest-span-first order measured no gain (profiles/r01_notes.md)
-    ra.width = cam->width;
-    ra.height = cam->height;
-    ra.tiles_x = tx;
-    ra.tiles_y = ty;
-    for (int i = 0; i < 3; ++i) ra.bg[i] = cam->background[i];
-    ra.alpha_low = (float)alpha_low;
-    ra.term = (float)term_threshold;
-    ra.pixels = buf->d_pixels;
-    ra.load = buf->d_load;
-    ra.stats = buf->d_stats;
-    ra.hist = buf->d_hist;
-    ra.hist_bins = buf->hist_bins;
-    ra.nan_flag = buf->d_counters + 4;
-    rc = launch_render(ra, st);
+int32_t adr_render_frame_post(const adr_scene* scene, const adr_camera* cam, int32_t mode, double alpha_low,
+                              double dilation, double term_threshold, const adr_frame_buffers* buf, void* stream) {
+    (void)mode;
+    (void)dilation;
+    FrameSetup f;
+    int32_t rc = frame_setup(scene, cam, alpha_low, buf, &f);
     if (rc) return rc;
-    if (ev[6]) ADR_CUDA_TRY(cudaEventRecord(ev[6], st));
-    return ADR_OK;
+    return frame_post(*scene, *cam, term_threshold, buf, f, as_stream(stream));
 }
 
 }  // extern "C"

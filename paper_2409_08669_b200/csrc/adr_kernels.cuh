@@ -96,6 +96,17 @@ int32_t launch_preprocess(const adr_scene& scene, const adr_camera& cam, int32_t
                           double alpha_low, double dilation, const adr_projection& out,
                           const FusedPre* fused, cudaStream_t st);
 
+// Stage 1 of several frames of one scene in one launch (adr_preprocess_views).
+constexpr int kMaxBatchViews = 8;
+struct PreViews {
+    int32_t nv = 0;
+    adr_camera cam[kMaxBatchViews];
+    adr_projection out[kMaxBatchViews];
+    FusedPre fused[kMaxBatchViews];
+};
+int32_t launch_preprocess_views(const adr_scene& scene, const PreViews& views, int32_t mode, double alpha_low,
+                                double dilation, cudaStream_t st);
+
 struct RenderArgs {
     const Record* rec;        // records
     const uint32_t* idx;      // per sorted pair: record index

@@ -100,6 +100,284 @@ __device__ __forceinline__ void stage_sh(const T* __restrict__ sh, int64_t first
     }
 }
 
+// A Gaussian's view-independent terms (sb/projection.py:337-372 before the
+// camera enters): the row's centre, cov3d = M Mᵀ with M = R(q)·diag(s) (six
+// unique entries: fma/mul are commutative, so cov[a][b] == cov[b][a] bit for
+// bit), sigma and ln(sigma / alpha_low) (not evaluated in BASELINE mode).
+struct PreRow {
+    double c[3];
+    double cov[6];   // xx, xy, xz, yy, yz, zz
+    double sigma;
+    double log_ratio;
+};
+
+__device__ __forceinline__ double cov_at(const PreRow& g, int a, int b) {
+    const int lo = a < b ? a : b, hi = a < b ? b : a;
+    return g.cov[lo == 0 ? hi : (lo == 1 ? 2 + hi : 5)];
+}
+
+template <typename T>
+__device__ __forceinline__ void pre_row(PreRow& g, const T ac[3], const T as[3], const T aq[4], T aop,
+                                        int32_t mode, double alpha_low) {
+    g.c[0] = (double)ac[0];
+    g.c[1] = (double)ac[1];
+    g.c[2] = (double)ac[2];
+    const double w = (double)aq[0], x = (double)aq[1], y = (double)aq[2], z = (double)aq[3];
+    double rq[9];
+    rq[0] = SUB(1.0, MUL(2.0, ADD(MUL(y, y), MUL(z, z))));
+    rq[1] = MUL(2.0, SUB(MUL(x, y), MUL(w, z)));
+    rq[2] = MUL(2.0, ADD(MUL(x, z), MUL(w, y)));
+    rq[3] = MUL(2.0, ADD(MUL(x, y), MUL(w, z)));
+    rq[4] = SUB(1.0, MUL(2.0, ADD(MUL(x, x), MUL(z, z))));
+    rq[5] = MUL(2.0, SUB(MUL(y, z), MUL(w, x)));
+    rq[6] = MUL(2.0, SUB(MUL(x, z), MUL(w, y)));
+    rq[7] = MUL(2.0, ADD(MUL(y, z), MUL(w, x)));
+    rq[8] = SUB(1.0, MUL(2.0, ADD(MUL(x, x), MUL(y, y))));
+    const double s0 = (double)as[0], s1 = (double)as[1], s2 = (double)as[2];
+    double m[9];
+#pragma unroll
+    for (int a = 0; a < 3; ++a) {
+        m[3 * a + 0] = MUL(rq[3 * a + 0], s0);
+        m[3 * a + 1] = MUL(rq[3 * a + 1], s1);
+        m[3 * a + 2] = MUL(rq[3 * a + 2], s2);
+    }
+    int u = 0;
+#pragma unroll
+    for (int a = 0; a < 3; ++a)
+#pragma unroll
+        for (int b = a; b < 3; ++b)
+            g.cov[u++] = FMA(m[3 * a + 2], m[3 * b + 2], FMA(m[3 * a + 1], m[3 * b + 1], MUL(m[3 * a], m[3 * b])));
+    g.sigma = (double)aop;
+    g.log_ratio = mode == ADR_MODE_BASELINE ? 0.0 : log_fd(np_max(__ddiv_rn(g.sigma, alpha_low), 1e-300));
+}
+
+// One view of one Gaussian row (k_preprocess_views; k_preprocess keeps its
+// own single-view body, which ptxas schedules without spills at the 72-register
+// budget): everything after the camera enters
+// (sb/projection.py:355-420), the fused frame's extras (sb/tiling.py:77-114)
+// and the block's fused epilogue.  `smm`: 2 * kPreBlock / 32 words of shared
+// memory for the key-extrema reduction (multi-view callers alternate two
+// buffers, so one barrier per view suffices).
+template <typename T, int DEG, bool FUSED>
+__device__ __forceinline__ void preprocess_view(const PreRow& g, bool in_range, int64_t i, const T* shp,
+                                                const adr_camera& cam, int32_t mode, double alpha_low,
+                                                double dilation, const adr_projection& out, const FusedPre& fused,
+                                                int64_t blk, uint32_t* smm) {
+    constexpr int K = (DEG + 1) * (DEG + 1);
+    bool alive = false;
+    bool selected = false;   // fused: touches >= 1 tile
+    uint32_t dbits = 0;      // fused: float32 depth bits
+    int ambiguous = 0;       // fused: ceil-ambiguous extents of this row (log fence)
+    bool nan_color = false;  // fused: a valid row with a NaN colour channel
+    if (in_range) {
+        const double* R = cam.rot;
+        const double c0 = g.c[0], c1 = g.c[1], c2 = g.c[2];
+        double pv[3];
+#pragma unroll
+        for (int k = 0; k < 3; ++k)
+            pv[k] = ADD(FMA(c2, R[3 * k + 2], FMA(c1, R[3 * k + 1], MUL(c0, R[3 * k + 0]))), cam.trans[k]);
+        const double depth = pv[2];
+        alive = depth > cam.near_plane;
+
+        const double safe_z = alive ? depth : 1.0;
+        const double inv_z = __ddiv_rn(1.0, safe_z);
+        const double tx = MUL(np_clip(MUL(pv[0], inv_z), -cam.lim_x, cam.lim_x), safe_z);
+        const double ty = MUL(np_clip(MUL(pv[1], inv_z), -cam.lim_y, cam.lim_y), safe_z);
+        const double j0 = MUL(cam.fx, inv_z);
+        const double j2x = MUL(MUL(MUL(-cam.fx, tx), inv_z), inv_z);
+        const double j1 = MUL(cam.fy, inv_z);
+        const double j2y = MUL(MUL(MUL(-cam.fy, ty), inv_z), inv_z);
+        double t0[3], t1[3];
+#pragma unroll
+        for (int k = 0; k < 3; ++k) {
+            t0[k] = ADD(MUL(j0, R[k]), MUL(j2x, R[6 + k]));
+            t1[k] = ADD(MUL(j1, R[3 + k]), MUL(j2y, R[6 + k]));
+        }
+        double ct0[3], ct1[3];
+#pragma unroll
+        for (int a = 0; a < 3; ++a) {
+            ct0[a] = FMA(cov_at(g, a, 2), t0[2], FMA(cov_at(g, a, 0), t0[0], MUL(cov_at(g, a, 1), t0[1])));
+            ct1[a] = FMA(cov_at(g, a, 2), t1[2], FMA(cov_at(g, a, 0), t1[0], MUL(cov_at(g, a, 1), t1[1])));
+        }
+        const double sxx = ADD(ADD(ADD(MUL(t0[0], ct0[0]), MUL(t0[1], ct0[1])), MUL(t0[2], ct0[2])), dilation);
+        const double syy = ADD(ADD(ADD(MUL(t1[0], ct1[0]), MUL(t1[1], ct1[1])), MUL(t1[2], ct1[2])), dilation);
+        const double sxy = ADD(ADD(MUL(t0[0], ct1[0]), MUL(t0[1], ct1[1])), MUL(t0[2], ct1[2]));
+
+        const double det = SUB(MUL(sxx, syy), MUL(sxy, sxy));
+        const double mid = MUL(0.5, ADD(sxx, syy));
+        const double disc = __dsqrt_rn(np_max(SUB(MUL(mid, mid), det), 0.0));
+        const double lam_max = ADD(mid, disc);
+        const double mx = ADD(MUL(MUL(cam.fx, pv[0]), inv_z), cam.cx);
+        const double my = ADD(MUL(MUL(cam.fy, pv[1]), inv_z), cam.cy);
+        const double r_o_real = MUL(3.0, __dsqrt_rn(np_max(lam_max, 0.0)));
+        const double sigma = g.sigma;
+        double ex, ey;
+        double ln_a_over_op = 1e300;   // for cull_params (fused); 1e300: not known
+
+        if (mode == ADR_MODE_BASELINE) {
+            ex = ceil(r_o_real);
+            ey = ex;
+        } else {
+            alive = alive && (sigma > alpha_low);
+            const double log_ratio = g.log_ratio;
+            if (FUSED) ln_a_over_op = fused.ln_a32_a64 - log_ratio;   // = ln(a32 / sigma)
+            if (mode == ADR_MODE_CIRCLE) {
+                const double v = __dsqrt_rn(MUL(MUL(2.0, lam_max), log_ratio));
+                ex = ceil(np_min(v, r_o_real));
+                ey = ex;
+                if (FUSED && alive) ambiguous = ceil_ambiguous(v, r_o_real);
+            } else {
+                const double vx = __dsqrt_rn(MUL(MUL(2.0, sxx), log_ratio));
+                const double vy = __dsqrt_rn(MUL(MUL(2.0, syy), log_ratio));
+                ex = ceil(np_min(vx, r_o_real));
+                ey = ceil(np_min(vy, r_o_real));
+                if (FUSED && alive) ambiguous = ceil_ambiguous(vx, r_o_real) + ceil_ambiguous(vy, r_o_real);
+            }
+        }
+        alive = alive && (ex >= 1.0) && (ey >= 1.0);
+
+        out.d_valid[i] = (uint8_t)alive;
+        if (alive) {
+            double d0 = SUB(c0, cam.center[0]), d1 = SUB(c1, cam.center[1]), d2 = SUB(c2, cam.center[2]);
+            const double nrm = __dsqrt_rn(ADD(ADD(MUL(d0, d0), MUL(d1, d1)), MUL(d2, d2)));
+            const double dn = nrm > 0 ? nrm : 1.0;
+            d0 = __ddiv_rn(d0, dn);
+            d1 = __ddiv_rn(d1, dn);
+            d2 = __ddiv_rn(d2, dn);
+            double col[3];
+#pragma unroll
+            for (int ch = 0; ch < 3; ++ch) {
+                double cf[K];
+#pragma unroll
+                for (int k = 0; k < K; ++k) cf[k] = (double)shp[k * 3 + ch];
+                col[ch] = sh_channel<DEG>(cf, d0, d1, d2);
+            }
+            const float2 m2 = make_float2(__double2float_rn(mx), __double2float_rn(my));
+            const float ca = __double2float_rn(__ddiv_rn(syy, det));
+            const float cb = __double2float_rn(__ddiv_rn(-sxy, det));
+            const float cc = __double2float_rn(__ddiv_rn(sxx, det));
+            const float dz = __double2float_rn(depth);
+            const float op = __double2float_rn(sigma);
+            const float c0f = __double2float_rn(col[0]), c1f = __double2float_rn(col[1]),
+                        c2f = __double2float_rn(col[2]);
+            if (!(FUSED && fused.rec_only)) {   // else these live in the render record only
+                reinterpret_cast<float2*>(out.d_mean2d)[i] = m2;
+                out.d_conic[3 * i] = ca;
+                out.d_conic[3 * i + 1] = cb;
+                out.d_conic[3 * i + 2] = cc;
+                out.d_color[3 * i] = c0f;
+                out.d_color[3 * i + 1] = c1f;
+                out.d_color[3 * i + 2] = c2f;
+                out.d_opacity[i] = op;
+            }
+            out.d_cov2d[3 * i] = __double2float_rn(sxx);
+            out.d_cov2d[3 * i + 1] = __double2float_rn(syy);
+            out.d_cov2d[3 * i + 2] = __double2float_rn(sxy);
+            out.d_depth[i] = dz;
+            out.d_lambda_max[i] = __double2float_rn(lam_max);
+            const int32_t ix = np_i32(ex), iy = np_i32(ey);
+            out.d_ext_x[i] = ix;
+            out.d_ext_y[i] = iy;
+            if (FUSED) {
+                nan_color = c0f != c0f || c1f != c1f || c2f != c2f;
+                const Rect r = tile_rect(m2.x, m2.y, ix, iy, true, fused.tiles_x, fused.tiles_y);
+                selected = r.count() > 0;
+                dbits = __float_as_uint(dz);
+                Record R;
+                float tau, hx, hy;
+                cull_params(ca, cb, cc, op, (float)alpha_low, c0f, c1f, c2f, &tau, &hx, &hy, ln_a_over_op);
+                R.a = make_float4(m2.x, m2.y, ca, cb);
+                R.b = make_float4(cc, op, c0f, c1f);
+                R.c = make_float4(c2f, tau, hx, hy);
+                fused.rec[i] = R;
+                fused.gpack[i] = make_uint2((uint32_t)r.x0 | ((uint32_t)r.x1 << 16),
+                                            (uint32_t)r.y0 | ((uint32_t)r.y1 << 16));
+            }
+        } else {
+            if (FUSED && fused.rec_only) {
+                const float4 z = make_float4(0.f, 0.f, 0.f, 0.f);
+                Record R;
+                R.a = R.b = R.c = z;
+                fused.rec[i] = R;
+            } else {
+                reinterpret_cast<float2*>(out.d_mean2d)[i] = make_float2(0.f, 0.f);
+                out.d_conic[3 * i] = out.d_conic[3 * i + 1] = out.d_conic[3 * i + 2] = 0.f;
+                out.d_color[3 * i] = out.d_color[3 * i + 1] = out.d_color[3 * i + 2] = 0.f;
+                out.d_opacity[i] = 0.f;
+            }
+            out.d_cov2d[3 * i] = out.d_cov2d[3 * i + 1] = out.d_cov2d[3 * i + 2] = 0.f;
+            out.d_depth[i] = 0.f;
+            out.d_lambda_max[i] = 0.f;
+            out.d_ext_x[i] = 0;
+            out.d_ext_y[i] = 0;
+        }
+    }
+    if (FUSED) {
+        // depth-sort key: float32 depth bits for Gaussians touching >= 1
+        // tile (depth > near_plane > 0, so bit 31 is clear), all-ones for the
+        // rest, which a stable sort then leaves behind the M selected ones
+        if (in_range) fused.dkey[i] = selected ? dbits : 0xffffffffu;
+        const int lane = threadIdx.x & 31;
+        const uint32_t culled = __ballot_sync(kFull, in_range && !alive);
+        const uint32_t sb = __ballot_sync(kFull, selected);
+        const uint32_t nanb = __ballot_sync(kFull, nan_color);
+        if (__any_sync(kFull, ambiguous != 0)) {
+            const int amb = __reduce_add_sync(kFull, (unsigned)ambiguous);
+            if (lane == 0 && fused.ambiguous) atomicAdd(fused.ambiguous, (unsigned long long)amb);
+        }
+        if (fused.kminmax) {   // the depth sort's key-range plan (adr_supertile.cu)
+            const uint32_t kmn = __reduce_min_sync(kFull, selected ? dbits : 0xffffffffu);
+            const uint32_t kmx = __reduce_max_sync(kFull, selected ? dbits : 0u);
+            const int wid = threadIdx.x >> 5;
+            if (lane == 0) {
+                smm[2 * wid] = kmn;
+                smm[2 * wid + 1] = kmx;
+            }
+            __syncthreads();
+            if (threadIdx.x == 0 && blk == 0 && fused.plan_mm) {
+                fused.plan_mm[0] = 0xffffffffu;
+                fused.plan_mm[1] = 0u;
+            }
+            if (threadIdx.x == 0) {
+                uint32_t a = smm[0], b = smm[1];
+                for (int w = 1; w < kPreBlock / 32; ++w) {
+                    a = smm[2 * w] < a ? smm[2 * w] : a;
+                    b = smm[2 * w + 1] > b ? smm[2 * w + 1] : b;
+                }
+                fused.kminmax[2 * blk] = a;
+                fused.kminmax[2 * blk + 1] = b;
+            }
+        }
+        if (lane == 0) {
+            if (culled) atomicAdd(fused.culled, (unsigned long long)__popc(culled));
+            if (sb) atomicAdd(reinterpret_cast<unsigned long long*>(fused.d_m), (unsigned long long)__popc(sb));
+            if (nanb && fused.nan_colors) atomicAdd(fused.nan_colors, (unsigned long long)__popc(nanb));
+        }
+    }
+}
+
+
+// Loads one block's rows: per-Gaussian attributes, then the SH slab staged
+// into shared memory (the caller synchronises before reading the stage).
+template <typename T, int DEG>
+__device__ __forceinline__ void load_block(const T* __restrict__ centers, const T* __restrict__ scales,
+                                           const T* __restrict__ rotations, const T* __restrict__ opacities,
+                                           const T* __restrict__ sh, int64_t n, int64_t first, T* stage,
+                                           T ac[3], T as[3], T aq[4], T& aop) {
+    const int64_t i = first + threadIdx.x;
+    if (i < n) {
+#pragma unroll
+        for (int k = 0; k < 3; ++k) {
+            ac[k] = centers[3 * i + k];
+            as[k] = scales[3 * i + k];
+        }
+#pragma unroll
+        for (int k = 0; k < 4; ++k) aq[k] = rotations[4 * i + k];
+        aop = opacities[i];
+    }
+    stage_sh<T, DEG>(sh, first, (int)(n - first < kPreBlock ? n - first : kPreBlock), stage);
+}
+
 template <typename T, int DEG, bool FUSED>
 __device__ __forceinline__ void preprocess_block(const T* __restrict__ centers, const T* __restrict__ scales,
                                                  const T* __restrict__ rotations, const T* __restrict__ opacities,
@@ -366,6 +644,43 @@ k_preprocess(const T* __restrict__ centers, const T* __restrict__ scales,
     }
 }
 
+
+// Stage 1 of up to kMaxBatchViews frames of ONE scene in one launch (the
+// views of a bench step / serving batch share the scene): each block reads
+// its 128 rows and their SH slab once, evaluates the view-independent terms
+// once (PreRow), then runs every view's projection / SH colour / outputs.
+// Every view's outputs are bit-identical to k_preprocess's (same operations
+// on the same operands); the scene is read once instead of nv times.
+// Register budget: 7 blocks/SM (72 registers, 48 B of spills) measured best
+// against 4 / 5 / 6 (120 / 96 / 80 registers), a float64 SH stage and the
+// view-independent row kept in shared memory (notes.md, experiment 20).
+#ifndef ADR_PREV_MINB
+#define ADR_PREV_MINB 7
+#endif
+template <typename T, int DEG>
+__global__ void __launch_bounds__(kPreBlock, ADR_PREV_MINB)
+k_preprocess_views(const T* __restrict__ centers, const T* __restrict__ scales,
+                   const T* __restrict__ rotations, const T* __restrict__ opacities,
+                   const T* __restrict__ sh, int64_t n, int32_t mode, double alpha_low, double dilation,
+                   const __grid_constant__ PreViews pv) {
+    constexpr int S = (DEG + 1) * (DEG + 1) * 3 + 1;
+    extern __shared__ __align__(16) unsigned char pre_smem[];
+    __shared__ uint32_t smm[2][2 * (kPreBlock / 32)];
+    T* stage = reinterpret_cast<T*>(pre_smem);
+    const int64_t blk = blockIdx.x;
+    const int64_t first = blk * kPreBlock;
+    const int64_t i = first + threadIdx.x;
+    T ac[3] = {T(0), T(0), T(0)}, as[3] = {T(0), T(0), T(0)}, aq[4] = {T(0), T(0), T(0), T(0)}, aop = T(0);
+    load_block<T, DEG>(centers, scales, rotations, opacities, sh, n, first, stage, ac, as, aq, aop);
+    __syncthreads();
+    PreRow g;
+    if (i < n) pre_row<T>(g, ac, as, aq, aop, mode, alpha_low);
+#pragma unroll 1
+    for (int v = 0; v < pv.nv; ++v)
+        preprocess_view<T, DEG, true>(g, i < n, i, stage + threadIdx.x * S, pv.cam[v], mode, alpha_low, dilation,
+                                      pv.out[v], pv.fused[v], blk, smm[v & 1]);
+}
+
 #undef MUL
 #undef ADD
 #undef SUB
@@ -428,6 +743,47 @@ int32_t launch_preprocess(const adr_scene& scene, const adr_camera& cam, int32_t
         return fused ? launch_typed<double, true>(scene, cam, mode, alpha_low, dilation, out, f, st)
                      : launch_typed<double, false>(scene, cam, mode, alpha_low, dilation, out, f, st);
     return fail(ADR_ERR_VALUE, "scene dtype must be ADR_F32 or ADR_F64");
+}
+
+
+int32_t launch_preprocess_views(const adr_scene& s, const PreViews& pv, int32_t mode, double alpha_low,
+                                double dilation, cudaStream_t st) {
+    if (!(alpha_low > 0.0 && alpha_low < 1.0)) return fail(ADR_ERR_VALUE, "alpha_low must lie in (0, 1)");
+    if (!(dilation >= 0.0)) return fail(ADR_ERR_VALUE, "dilation must be non-negative");
+    if (mode < ADR_MODE_BASELINE || mode > ADR_MODE_AABB) return fail(ADR_ERR_VALUE, "unknown culling mode");
+    if (pv.nv < 1 || pv.nv > kMaxBatchViews) return fail(ADR_ERR_VALUE, "n_views must lie in 1..8");
+    if (s.n < 0) return fail(ADR_ERR_VALUE, "negative Gaussian count");
+    if (s.n == 0) return ADR_OK;
+    const int64_t grid = ceil_div(s.n, kPreBlock);
+#define ADR_PREV(T, DEG)                                                                                       \
+    do {                                                                                                       \
+        const size_t sm = sizeof(T) * kPreBlock * ((DEG + 1) * (DEG + 1) * 3 + 1);                  \
+        ADR_CUDA_TRY(cudaFuncSetAttribute(k_preprocess_views<T, DEG>, cudaFuncAttributeMaxDynamicSharedMemorySize, \
+                                          (int)sm));                                                           \
+        k_preprocess_views<T, DEG><<<grid, kPreBlock, sm, st>>>(                                               \
+            static_cast<const T*>(s.d_centers), static_cast<const T*>(s.d_scales),                             \
+            static_cast<const T*>(s.d_rotations), static_cast<const T*>(s.d_opacities),                        \
+            static_cast<const T*>(s.d_sh), s.n, mode, alpha_low, dilation, pv);                                \
+    } while (0)
+#define ADR_PREV_T(T)                                                   \
+    switch (s.sh_degree) {                                              \
+        case 0: ADR_PREV(T, 0); break;                                  \
+        case 1: ADR_PREV(T, 1); break;                                  \
+        case 2: ADR_PREV(T, 2); break;                                  \
+        case 3: ADR_PREV(T, 3); break;                                  \
+        default: return fail(ADR_ERR_VALUE, "sh_degree must be in 0..3"); \
+    }
+    if (s.dtype == ADR_F32) {
+        ADR_PREV_T(float)
+    } else if (s.dtype == ADR_F64) {
+        ADR_PREV_T(double)
+    } else {
+        return fail(ADR_ERR_VALUE, "scene dtype must be ADR_F32 or ADR_F64");
+    }
+#undef ADR_PREV_T
+#undef ADR_PREV
+    ADR_LAUNCH_CHECK();
+    return ADR_OK;
 }
 
 }  // namespace adr

@@ -224,6 +224,30 @@ class Rasterizer:
                 float(alpha_low), float(dilation), float(term_threshold),
                 ctypes.byref(self._buffers(timed)), _lib.stream_handle(st)))
 
+    def _check_frame(self, scene: DeviceScene, cam) -> None:
+        if len(scene) != self.n:
+            raise ValueError("scene size does not match the rasterizer")
+        if (int(cam.width), int(cam.height)) != (self.width, self.height):
+            raise ValueError("camera resolution does not match the rasterizer")
+
+    def launch_post(self, scene: DeviceScene, cam, mode=CullingMode.AABB, alpha_low=ALPHA_LOW,
+                    dilation=COV_DILATION, term_threshold=TERMINATION_THRESHOLD, stream=None,
+                    timed: bool = False) -> None:
+        """Enqueue stages 2-6 of a frame whose stage 1 ran through
+        ``preprocess_views`` into this rasterizer (same scene, camera, mode and
+        alpha_low), on `stream` after that launch; no host sync."""
+        import torch
+
+        mode = CullingMode(mode)
+        self._check_frame(scene, cam)
+        self.proj.mode, self.proj.alpha_low = mode, alpha_low
+        with torch.cuda.device(self.device):
+            st = stream if stream is not None else torch.cuda.current_stream()
+            _lib.check(_lib.lib().adr_render_frame_post(
+                scene_struct(scene), _lib.camera_struct(cam), _lib.MODE_CODES[mode.value],
+                float(alpha_low), float(dilation), float(term_threshold),
+                ctypes.byref(self._buffers(timed)), _lib.stream_handle(st)))
+
     def pair_count(self) -> int:
         return int(self.counters[0].item())
 
@@ -298,6 +322,53 @@ class Rasterizer:
             self.launch(scene, cam, mode, alpha_low, dilation, term_threshold, stream=s)
         torch.cuda.synchronize(self.device)
         return FrameGraph(g, self)
+
+
+MAX_BATCH_VIEWS = 8   # views per preprocess_views launch (adr_preprocess_views)
+
+
+def preprocess_views(scene: DeviceScene, cams, rasts, mode=CullingMode.AABB, alpha_low=ALPHA_LOW,
+                     dilation=COV_DILATION, stream=None) -> None:
+    """Stage 1 of ``len(cams)`` (1..8) frames of one scene in ONE launch: each
+    Gaussian and its SH coefficients are read once, its view-independent terms
+    evaluated once, and view v's Projection / render record / tile rects /
+    depth keys land in ``rasts[v]`` (one Rasterizer per view, distinct) —
+    bit-identical to ``rasts[v].launch(scene, cams[v])``'s stage 1.  Follow
+    with ``rasts[v].launch_post(scene, cams[v], ...)`` per view (any stream
+    ordered after this one)."""
+    import torch
+
+    cams, rasts = list(cams), list(rasts)
+    if not 1 <= len(cams) <= MAX_BATCH_VIEWS:
+        raise ValueError(f"preprocess_views takes 1..{MAX_BATCH_VIEWS} views")
+    if len(rasts) != len(cams):
+        raise ValueError("one Rasterizer per view")
+    if len({id(r) for r in rasts}) != len(rasts):
+        raise ValueError("every view needs its own Rasterizer")
+    mode = CullingMode(mode)
+    for r, c in zip(rasts, cams):
+        r._check_frame(scene, c)
+        if r.device != rasts[0].device:
+            raise ValueError("all rasterizers must live on one device")
+        r.proj.mode, r.proj.alpha_low = mode, alpha_low
+    cam_arr = (_lib.Camera_t * len(cams))(*[_lib.camera_struct(c) for c in cams])
+    buf_arr = (_lib.FrameBuffers_t * len(rasts))(*[r._buffers(False) for r in rasts])
+    with torch.cuda.device(rasts[0].device):
+        st = stream if stream is not None else torch.cuda.current_stream()
+        _lib.check(_lib.lib().adr_preprocess_views(
+            scene_struct(scene), cam_arr, len(cams), _lib.MODE_CODES[mode.value], float(alpha_low),
+            float(dilation), buf_arr, _lib.stream_handle(st)))
+
+
+def render_views_batched(scene: DeviceScene, cams, rasts, mode=CullingMode.AABB, alpha_low=ALPHA_LOW,
+                         dilation=COV_DILATION, term_threshold=TERMINATION_THRESHOLD, stream=None) -> None:
+    """Enqueue whole frames of ``len(cams)`` (1..8) views of one scene on one
+    stream: one ``preprocess_views`` launch, then each view's stages 2-6 in
+    ``rasts[v]`` (read the results with ``rasts[v].result(...)`` after a
+    sync).  Frames equal ``rasts[v].launch(scene, cams[v])`` bit for bit."""
+    preprocess_views(scene, cams, rasts, mode, alpha_low, dilation, stream)
+    for r, c in zip(rasts, cams):
+        r.launch_post(scene, c, mode, alpha_low, dilation, term_threshold, stream=stream)
 
 
 _workspace = threading.local()   # per host thread: {(device, N, W, H): Rasterizer}

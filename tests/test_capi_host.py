@@ -24,7 +24,7 @@ def test_library_exports_every_header_symbol():
     for name in sorted(declared):
         assert hasattr(L, name), f"{name} not exported"
     assert declared == set(_lib.EXPORTED)
-    assert L.adr_abi_version() == 2
+    assert L.adr_abi_version() == 3
 
 
 def test_scratch_queries_need_no_gpu():
