@@ -224,33 +224,48 @@ class ViewRenderer:
     """Renders a batch of cameras of one resident scene with several views in
     flight (BASELINE configs[3]/[4]).
 
-    Each in-flight slot owns a ``Rasterizer`` (persistent buffers) and a CUDA
-    stream; view i renders in slot i mod K, so frames of different views
-    overlap on the GPU while every frame stays a fixed kernel sequence.
-    Results are copied into batch tensors on the slot's stream; a view whose
-    pairs exceed its slot's capacity is re-rendered with larger buffers, so
-    every output equals a single-view ``run_pipeline`` bit for bit.
+    Views are taken in groups of ``batch_views`` (<= 8): one
+    ``preprocess_views`` launch runs stage 1 of the whole group (the scene is
+    read once), then each view's stages 2-6 run in its own ``Rasterizer``
+    slot on one of ``in_flight`` CUDA streams, so frames of different views
+    overlap on the GPU; two slot sets alternate, so group g+1's stage 1
+    overlaps group g's binning and render.  ``batch_views=1``: every view is
+    one whole-frame call, view i in slot i mod ``in_flight``.  Results are
+    copied into batch tensors on the slot's stream; a view whose pairs exceed
+    its slot's capacity is re-rendered with larger buffers, so every output
+    equals a single-view ``run_pipeline`` bit for bit.
     """
 
-    def __init__(self, scene, width: int, height: int, in_flight: int = 4, device=None):
+    def __init__(self, scene, width: int, height: int, in_flight: int = 4, device=None,
+                 batch_views: int = 8):
         import torch
 
-        from .pipeline import Rasterizer
+        from .pipeline import MAX_BATCH_VIEWS
         from .projection import as_device_scene
 
         self.scene = as_device_scene(scene, device)
         self.device = self.scene.device
         self.width, self.height = int(width), int(height)
         k = max(1, int(in_flight))
-        self.slots = [Rasterizer(self.width, self.height, len(self.scene), device=self.device, timing=False)
-                      for _ in range(k)]
+        self.batch = max(1, min(int(batch_views), MAX_BATCH_VIEWS))
+        self.slots = []
+        self._grow(k if self.batch == 1 else self.batch)
         self.streams = [torch.cuda.Stream(self.device) for _ in range(k)]
+        self.pre_streams = [torch.cuda.Stream(self.device) for _ in range(2)]
+
+    def _grow(self, n_slots: int) -> None:
+        from .pipeline import Rasterizer
+
+        while len(self.slots) < n_slots:
+            self.slots.append(Rasterizer(self.width, self.height, len(self.scene), device=self.device,
+                                         timing=False))
 
     def render(self, cams, mode="aabb", alpha_low=None):
         """-> (pixels (V,H,W,3) f32, load (V,H,W) i32, stats (V, 6) i64 in
         STATS_FIELDS order) as CUDA tensors."""
         import torch
 
+        from .pipeline import preprocess_views
         from .projection import ALPHA_LOW
 
         alpha_low = ALPHA_LOW if alpha_low is None else alpha_low
@@ -259,39 +274,75 @@ class ViewRenderer:
         pixels = torch.empty((v, self.height, self.width, 3), dtype=torch.float32, device=dev)
         load = torch.empty((v, self.height, self.width), dtype=torch.int32, device=dev)
         stats = torch.empty((v, len(STATS_FIELDS)), dtype=torch.int64, device=dev)
-        k = len(self.slots)
+        k = len(self.streams)
         main = torch.cuda.current_stream(dev)
         ev = torch.cuda.Event()
         ev.record(main)
-        for st in self.streams:
+        for st in self.streams + self.pre_streams:
             st.wait_event(ev)
 
-        def one(i):
-            r, st = self.slots[i % k], self.streams[i % k]
+        def copy_out(i, r):
+            pixels[i].copy_(r.pixels, non_blocking=True)
+            load[i].copy_(r.load, non_blocking=True)
+            stats[i, 0:2].copy_(r.counters[0:2], non_blocking=True)
+            stats[i, 2:4].copy_(r.stats[0:2], non_blocking=True)
+            mm = r.stats[2:3]   # packed (min, max) int32 pair
+            stats[i, 4] = mm & 0xFFFFFFFF
+            stats[i, 5] = (mm >> 32) & 0xFFFFFFFF
+
+        def one(i, r):   # a whole frame of view i in slot r
+            st = self.streams[i % k]
             with torch.cuda.stream(st):
                 r.launch(self.scene, cams[i], mode, alpha_low, stream=st)
-                pixels[i].copy_(r.pixels, non_blocking=True)
-                load[i].copy_(r.load, non_blocking=True)
-                stats[i, 0:2].copy_(r.counters[0:2], non_blocking=True)
-                stats[i, 2:4].copy_(r.stats[0:2], non_blocking=True)
-                mm = r.stats[2:3]   # packed (min, max) int32 pair
-                stats[i, 4] = mm & 0xFFFFFFFF
-                stats[i, 5] = (mm >> 32) & 0xFFFFFFFF
+                copy_out(i, r)
 
-        for i in range(v):
-            one(i)
-        for st in self.streams:
+        slot_of = {}
+        if self.batch == 1:
+            for i in range(v):
+                slot_of[i] = self.slots[i % k]
+                one(i, slot_of[i])
+        else:
+            b = self.batch
+            groups = [list(range(g, min(g + b, v))) for g in range(0, v, b)]
+            n_sets = min(2, len(groups))
+            self._grow(b * n_sets)
+            pending = [[] for _ in range(n_sets)]
+            for gi, grp in enumerate(groups):
+                ss = gi % n_sets
+                ps = self.pre_streams[ss]
+                for e in pending[ss]:
+                    ps.wait_event(e)
+                sl = [self.slots[ss * b + q] for q in range(len(grp))]
+                preprocess_views(self.scene, [cams[i] for i in grp], sl, mode, alpha_low, stream=ps)
+                pe = torch.cuda.Event()
+                pe.record(ps)
+                used = []
+                for q, i in enumerate(grp):
+                    slot_of[i] = sl[q]
+                    st = self.streams[i % k]
+                    st.wait_event(pe)
+                    with torch.cuda.stream(st):
+                        sl[q].launch_post(self.scene, cams[i], mode, alpha_low, stream=st)
+                        copy_out(i, sl[q])
+                    if st not in used:
+                        used.append(st)
+                pending[ss] = []
+                for st in used:
+                    e = torch.cuda.Event()
+                    e.record(st)
+                    pending[ss].append(e)
+        for st in self.streams + self.pre_streams:
             e = torch.cuda.Event()
             e.record(st)
             main.wait_event(e)
         torch.cuda.synchronize(dev)
-        # views that overflowed their slot: grow that slot, render again
-        caps = torch.tensor([self.slots[i % k].cap for i in range(v)], dtype=torch.int64)
+        # views that overflowed their slot: grow that slot, render the view again
+        caps = torch.tensor([slot_of[i].cap for i in range(v)], dtype=torch.int64)
         over = (stats[:, 0].cpu() > caps).nonzero().flatten().tolist()
         for i in over:
-            slot = self.slots[i % k]
+            slot = slot_of[i]
             slot.fit_capacity(int(stats[i, 0].item() * 1.25) + 1024)
-            one(i)
+            one(i, slot)
             torch.cuda.synchronize(dev)
         # the min/max halves are signed int32
         for c in (4, 5):
@@ -300,7 +351,7 @@ class ViewRenderer:
         return pixels, load, stats
 
 
-def render_views_sharded(scene, cams, in_flight: int = 4, group=None, dst: int = 0):
+def render_views_sharded(scene, cams, in_flight: int = 4, group=None, dst: int = 0, batch_views: int = 8):
     """Multi-GPU view-sharded rendering: this rank renders its contiguous
     slice of ``cams`` (``shard_views``) with a ``ViewRenderer`` and the frames
     plus stats are gathered to ``dst`` (``FrameGather``).  Returns
@@ -312,7 +363,7 @@ def render_views_sharded(scene, cams, in_flight: int = 4, group=None, dst: int =
     rank = dist.get_rank(group)
     views = list(shard_views(len(cams), world, rank))
     w, h = cams[0].width, cams[0].height
-    vr = ViewRenderer(scene, w, h, in_flight)
+    vr = ViewRenderer(scene, w, h, in_flight, batch_views=batch_views)
     fg = FrameGather(len(cams), h, w, vr.device, group=group, dst=dst)
     fg.begin()
     if views:

@@ -188,10 +188,13 @@ def test_fullsize_graph_replay_deterministic():
     assert torch.equal(rast.keys[:p0], keys0)
 
 
-def test_view_renderer_matches_single_view_frames():
-    """Views in flight (several Rasterizers on their own streams) give every
-    view exactly its single-view run_pipeline output; the overflow path
-    (a slot too small for a view) re-renders and still matches."""
+@pytest.mark.parametrize("batch_views", [1, 3, 8])
+def test_view_renderer_matches_single_view_frames(batch_views):
+    """Views in flight (several Rasterizers on their own streams; stage 1
+    batched over `batch_views` views, two slot sets alternating when there
+    are several groups) give every view exactly its single-view run_pipeline
+    output; the overflow path (a slot too small for a view) re-renders and
+    still matches."""
     import torch
 
     import paper_2409_08669_b200 as ab
@@ -202,7 +205,7 @@ def test_view_renderer_matches_single_view_frames():
                             sh_degree=1, float32=True)
     ds = ab.DeviceScene.from_arrays(a, 1, "cuda", torch.float32)
     cams = orbit_cameras(7, 320, 200, radius=2.6, background=(0.1, 0.2, 0.3))
-    vr = ViewRenderer(ds, 320, 200, in_flight=3)
+    vr = ViewRenderer(ds, 320, 200, in_flight=3, batch_views=batch_views)
     for s in vr.slots[1:]:
         s.cap = 0
         s._ensure_capacity(50_000)   # forces the overflow/re-render path for some views
