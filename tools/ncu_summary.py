@@ -17,7 +17,7 @@ M = [("gpu__time_duration.sum", "us"), ("dram__bytes_read.sum", "rd"), ("dram__b
      ("sm__pipe_fma_cycles_active.avg.pct_of_peak_sustained_active", "fma%"),
      ("launch__registers_per_thread", "regs")]
 SCALE = {"byte": 1e-6, "Kbyte": 1e-3, "Mbyte": 1.0, "Gbyte": 1e3, "nsecond": 1e-3, "usecond": 1.0,
-         "msecond": 1e3}
+         "msecond": 1e3, "ms": 1e3, "us": 1.0, "ns": 1e-3, "MB": 1.0, "GB": 1e3, "KB": 1e-3, "B": 1e-6}
 
 
 def main(rep, peak="6536.4"):
