@@ -78,12 +78,17 @@ def parse():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--cpu-budget", type=float, default=12.0, help="seconds of sampled CPU render")
-    ap.add_argument("--streams", type=int, default=4,
+    ap.add_argument("--streams", type=int, default=8,
                     help="views in flight per GPU: one Rasterizer + stream each (frames of different "
                          "views overlap; each frame is still one CUDA graph)")
-    ap.add_argument("--batch-views", type=int, default=8,
+    ap.add_argument("--batch-views", type=int, default=-1,
                     help="views per stage-1 launch (adr_preprocess_views: the scene is read once for the "
-                         "batch); 1 = one adr_render_frame graph per view")
+                         "batch); 1 = one adr_render_frame graph per view; -1 (default): 8 for scenes of "
+                         ">= 262144 Gaussians, else 1 (a 10k-Gaussian frame is launch-bound: notes.md "
+                         "experiment 21)")
+    ap.add_argument("--e2e-streams", type=int, default=4,
+                    help="views in flight in the e2e legs (single-view C-ABI frame calls; notes.md "
+                         "experiments 14 and 21)")
     return ap.parse_args()
 
 
@@ -335,6 +340,7 @@ def run_ours(args, cfg, rank, world, local):
     launches_per_frame = L.adr_kernel_launches() - before
     # views in flight: view j of this rank renders through slot j % K on its own stream
     n_fly = max(1, min(args.streams, max(n_mine, 1)))
+    n_e2e = max(1, min(args.e2e_streams, n_fly))   # views in flight in the e2e legs
     rasts = [rast] + [ab.Rasterizer(cfg["w"], cfg["h"], cfg["n"], device=dev, pair_capacity=rast.cap,
                                     timing=False) for _ in range(n_fly - 1)]
     streams = [torch.cuda.Stream(dev) for _ in range(n_fly)]
@@ -342,7 +348,8 @@ def run_ours(args, cfg, rank, world, local):
     # batched stage 1: groups of G consecutive views share one preprocess_views
     # launch (one scene read); two slot sets alternate so group g+1's stage 1
     # overlaps group g's binning + render
-    G = max(1, min(args.batch_views, ab.MAX_BATCH_VIEWS, max(n_mine, 1)))
+    bv = args.batch_views if args.batch_views > 0 else (ab.MAX_BATCH_VIEWS if cfg["n"] >= 262144 else 1)
+    G = max(1, min(bv, ab.MAX_BATCH_VIEWS, max(n_mine, 1)))
     groups = [list(range(i, min(i + G, n_mine))) for i in range(0, n_mine, G)] if G > 1 else []
     n_sets = min(2, len(groups))
     slots, pre_graphs, post_graphs, pre_streams = [], [], [], []
@@ -579,7 +586,7 @@ def run_ours(args, cfg, rank, world, local):
                 for st in streams:
                     st.wait_event(ready[bb])
                 for _ in range(views_per_step):
-                    k = j % n_fly
+                    k = j % n_e2e
                     rasts[k].launch(scenes[bb], cams[mine[j % n_mine]], mode=cfg["mode"], stream=streams[k])
                     with torch.cuda.stream(streams[k]):
                         slot_h[k][0].copy_(rasts[k].pixels, non_blocking=True)
@@ -606,7 +613,7 @@ def run_ours(args, cfg, rank, world, local):
             st.wait_event(b0)
         n_res = max(args.steps, 8)
         for s_ in range(n_res):
-            k = s_ % n_fly
+            k = s_ % n_e2e
             rasts[k].launch(ds, cams[mine[s_ % n_mine]], mode=cfg["mode"], stream=streams[k])
             with torch.cuda.stream(streams[k]):
                 slot_h[k][0].copy_(rasts[k].pixels, non_blocking=True)
@@ -668,7 +675,8 @@ def run_ours(args, cfg, rank, world, local):
                      "frame": (f"stage 1 of {G} views per launch (preprocess_views graph, scene read once per "
                                f"group), stages 2-6 a CUDA graph per view, no host sync" if groups else
                                "CUDA graph per view, no host sync"),
-                     "views_in_flight": n_fly, "batch_views": G if groups else 1})
+                     "views_in_flight": n_fly, "e2e_views_in_flight": n_e2e,
+                     "batch_views": G if groups else 1})
         line = {
             "metric": METRIC, "value": value, "unit": "frames/s", "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_per_step,

@@ -51,7 +51,7 @@ size_t frame_bytes(int64_t n, int32_t tx, int32_t ty, int64_t cap, FrameLayout* 
     l.rec_offset = c.used;
     l.rec = c.take<Record>(n);
     l.gpack = c.take<uint2>(n);
-    l.kminmax = c.take<uint32_t>(2 * ceil_div(n > 0 ? n : 1, 128));
+    l.kminmax = c.take<uint32_t>(2 * 4 * ceil_div(n > 0 ? n : 1, 128));   // per preprocess warp
     l.plan_mm = c.take<uint32_t>(2);
     l.tile_order = c.take<uint32_t>(n_tiles);
     l.binning_bytes = frame_binning_scratch(n, cap, tx, ty);

@@ -2,7 +2,7 @@
 // radix sort (stable, 8-bit digits) of the N depth keys with the identity as
 // values (sb/tiling.py:159-164 ordering: (float32 depth bits, index)).
 //
-//   k_ds_plan  : kPlanBlocks blocks reduce the preprocess's per-block key
+//   k_ds_plan  : kPlanBlocks blocks reduce the preprocess's per-warp key
 //                extrema into the key-range plan (adr_sort.cuh DepthPlan:
 //                24-bit keys t = key - kmin when they fit, three passes);
 //   k_ds_hist0 : the digit histogram of pass 0 (the raw low byte, equal to

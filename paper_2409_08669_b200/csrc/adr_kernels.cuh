@@ -84,7 +84,7 @@ struct FusedPre {
     int64_t* d_m = nullptr;                   // += number of Gaussians with pairs (zeroed)
     unsigned long long* nan_colors = nullptr; // += valid rows with a NaN colour channel
     unsigned long long* ambiguous = nullptr;  // += ceil-ambiguous extents (log fence)
-    uint32_t* kminmax = nullptr;              // per block: min and max depth key of the selected rows
+    uint32_t* kminmax = nullptr;              // per preprocess warp: min and max depth key of the selected rows
                                               // ([2 b] = min, [2 b + 1] = max; none: all-ones, 0)
     uint32_t* plan_mm = nullptr;              // the depth plan's (min, max), reset to (all-ones, 0) here
     bool rec_only = false;                    // mean2d / conic / opacity / color only in the record

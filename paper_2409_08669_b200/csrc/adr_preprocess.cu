@@ -155,14 +155,13 @@ __device__ __forceinline__ void pre_row(PreRow& g, const T ac[3], const T as[3],
 // own single-view body, which ptxas schedules without spills at the 72-register
 // budget): everything after the camera enters
 // (sb/projection.py:355-420), the fused frame's extras (sb/tiling.py:77-114)
-// and the block's fused epilogue.  `smm`: 2 * kPreBlock / 32 words of shared
-// memory for the key-extrema reduction (multi-view callers alternate two
-// buffers, so one barrier per view suffices).
+// and the warp's fused epilogue (no block barrier: warps of a block run their
+// views independently).
 template <typename T, int DEG, bool FUSED>
 __device__ __forceinline__ void preprocess_view(const PreRow& g, bool in_range, int64_t i, const T* shp,
                                                 const adr_camera& cam, int32_t mode, double alpha_low,
                                                 double dilation, const adr_projection& out, const FusedPre& fused,
-                                                int64_t blk, uint32_t* smm) {
+                                                int64_t blk) {
     constexpr int K = (DEG + 1) * (DEG + 1);
     bool alive = false;
     bool selected = false;   // fused: touches >= 1 tile
@@ -325,28 +324,16 @@ __device__ __forceinline__ void preprocess_view(const PreRow& g, bool in_range, 
             const int amb = __reduce_add_sync(kFull, (unsigned)ambiguous);
             if (lane == 0 && fused.ambiguous) atomicAdd(fused.ambiguous, (unsigned long long)amb);
         }
-        if (fused.kminmax) {   // the depth sort's key-range plan (adr_supertile.cu)
+        if (fused.kminmax) {   // the depth sort's key-range plan (adr_supertile.cu): per-warp extrema
             const uint32_t kmn = __reduce_min_sync(kFull, selected ? dbits : 0xffffffffu);
             const uint32_t kmx = __reduce_max_sync(kFull, selected ? dbits : 0u);
-            const int wid = threadIdx.x >> 5;
-            if (lane == 0) {
-                smm[2 * wid] = kmn;
-                smm[2 * wid + 1] = kmx;
-            }
-            __syncthreads();
             if (threadIdx.x == 0 && blk == 0 && fused.plan_mm) {
                 fused.plan_mm[0] = 0xffffffffu;
                 fused.plan_mm[1] = 0u;
             }
-            if (threadIdx.x == 0) {
-                uint32_t a = smm[0], b = smm[1];
-                for (int w = 1; w < kPreBlock / 32; ++w) {
-                    a = smm[2 * w] < a ? smm[2 * w] : a;
-                    b = smm[2 * w + 1] > b ? smm[2 * w + 1] : b;
-                }
-                fused.kminmax[2 * blk] = a;
-                fused.kminmax[2 * blk + 1] = b;
-            }
+            if (lane == 0)
+                reinterpret_cast<uint2*>(fused.kminmax)[blk * (kPreBlock / 32) + (threadIdx.x >> 5)] =
+                    make_uint2(kmn, kmx);
         }
         if (lane == 0) {
             if (culled) atomicAdd(fused.culled, (unsigned long long)__popc(culled));
@@ -592,29 +579,16 @@ __device__ __forceinline__ void preprocess_block(const T* __restrict__ centers, 
             const int amb = __reduce_add_sync(kFull, (unsigned)ambiguous);
             if (lane == 0 && fused.ambiguous) atomicAdd(fused.ambiguous, (unsigned long long)amb);
         }
-        if (fused.kminmax) {   // the depth sort's key-range plan (adr_supertile.cu)
-            __shared__ uint32_t smm[2 * (kPreBlock / 32)];
+        if (fused.kminmax) {   // the depth sort's key-range plan (adr_supertile.cu): per-warp extrema
             const uint32_t kmn = __reduce_min_sync(kFull, selected ? dbits : 0xffffffffu);
             const uint32_t kmx = __reduce_max_sync(kFull, selected ? dbits : 0u);
-            const int wid = threadIdx.x >> 5;
-            if (lane == 0) {
-                smm[2 * wid] = kmn;
-                smm[2 * wid + 1] = kmx;
-            }
-            __syncthreads();
             if (threadIdx.x == 0 && blk == 0 && fused.plan_mm) {
                 fused.plan_mm[0] = 0xffffffffu;
                 fused.plan_mm[1] = 0u;
             }
-            if (threadIdx.x == 0) {
-                uint32_t a = smm[0], b = smm[1];
-                for (int w = 1; w < kPreBlock / 32; ++w) {
-                    a = smm[2 * w] < a ? smm[2 * w] : a;
-                    b = smm[2 * w + 1] > b ? smm[2 * w + 1] : b;
-                }
-                fused.kminmax[2 * blk] = a;
-                fused.kminmax[2 * blk + 1] = b;
-            }
+            if (lane == 0)
+                reinterpret_cast<uint2*>(fused.kminmax)[blk * (kPreBlock / 32) + (threadIdx.x >> 5)] =
+                    make_uint2(kmn, kmx);
         }
         if (lane == 0) {
             if (culled) atomicAdd(fused.culled, (unsigned long long)__popc(culled));
@@ -665,7 +639,6 @@ k_preprocess_views(const T* __restrict__ centers, const T* __restrict__ scales,
                    const __grid_constant__ PreViews pv) {
     constexpr int S = (DEG + 1) * (DEG + 1) * 3 + 1;
     extern __shared__ __align__(16) unsigned char pre_smem[];
-    __shared__ uint32_t smm[2][2 * (kPreBlock / 32)];
     T* stage = reinterpret_cast<T*>(pre_smem);
     const int64_t blk = blockIdx.x;
     const int64_t first = blk * kPreBlock;
@@ -678,7 +651,7 @@ k_preprocess_views(const T* __restrict__ centers, const T* __restrict__ scales,
 #pragma unroll 1
     for (int v = 0; v < pv.nv; ++v)
         preprocess_view<T, DEG, true>(g, i < n, i, stage + threadIdx.x * S, pv.cam[v], mode, alpha_low, dilation,
-                                      pv.out[v], pv.fused[v], blk, smm[v & 1]);
+                                      pv.out[v], pv.fused[v], blk);
 }
 
 #undef MUL

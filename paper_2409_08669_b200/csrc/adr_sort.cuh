@@ -75,8 +75,8 @@ struct DepthPlan {
     const uint32_t* plan = nullptr;       // (min, max) selected depth key; reset by the preprocess
     int pass = 0;
     uint32_t* plan_out = nullptr;         // pass 0 upsweep: the extra blocks' atomic min / max target
-    const uint32_t* kminmax = nullptr;    // per preprocess block: (min, max) selected key
-    int64_t nkb = 0;                      // number of preprocess blocks
+    const uint32_t* kminmax = nullptr;    // per preprocess warp: (min, max) selected key
+    int64_t nkb = 0;                      // number of preprocess warps (4 per block)
 };
 
 constexpr int kPlanBlocks = 16;           // extra blocks of pass 0's upsweep that reduce the plan
@@ -110,7 +110,7 @@ __device__ __forceinline__ void plan_transform(K (&kr)[N], const DepthPlan& dp) 
 }
 
 // A plan block (pass 0 upsweep, the last kPlanBlocks blocks of the grid):
-// min / max over its slice of the preprocess blocks' extrema, merged with
+// min / max over its slice of the preprocess warps' extrema, merged with
 // two atomics.
 template <int BLOCK>
 __device__ __forceinline__ void plan_reduce(const DepthPlan& dp, int slice) {

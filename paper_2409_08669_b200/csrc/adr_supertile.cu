@@ -797,7 +797,7 @@ int32_t frame_binning_supertile(const FrameBinning& fb, cudaStream_t st) {
         dp.plan = fb.plan_mm;
         dp.plan_out = fb.plan_mm;
         dp.kminmax = fb.kminmax;
-        dp.nkb = ceil_div(n, 128);
+        dp.nkb = 4 * ceil_div(n, 128);   // one (min, max) per preprocess warp
     }
     int32_t rc = depth_sort_onesweep(fb.dkey, n, dp, fb.gpack, rinfo, ds_scratch, ds_bytes, st);
     if (rc) return rc;
