@@ -86,6 +86,11 @@ def parse():
                          "batch); 1 = one adr_render_frame graph per view; -1 (default): 8 for scenes of "
                          ">= 262144 Gaussians, else 1 (a 10k-Gaussian frame is launch-bound: notes.md "
                          "experiment 21)")
+    ap.add_argument("--slot-sets", type=int, default=0,
+                    help="batched stage 1: slot sets the groups alternate over (2: a group's stage 1 "
+                         "overlaps the previous group's frames, also across steps); 0 (default): 2 when "
+                         "a step has several groups, else 1 (garden: 1 set 832-837 vs 2 sets 822-829 "
+                         "frames/s; truck the other way round, 1933 vs 1967: notes.md experiment 22)")
     ap.add_argument("--e2e-streams", type=int, default=4,
                     help="views in flight in the e2e legs (single-view C-ABI frame calls; notes.md "
                          "experiments 14 and 21)")
@@ -351,7 +356,9 @@ def run_ours(args, cfg, rank, world, local):
     bv = args.batch_views if args.batch_views > 0 else (ab.MAX_BATCH_VIEWS if cfg["n"] >= 262144 else 1)
     G = max(1, min(bv, ab.MAX_BATCH_VIEWS, max(n_mine, 1)))
     groups = [list(range(i, min(i + G, n_mine))) for i in range(0, n_mine, G)] if G > 1 else []
-    n_sets = min(2, len(groups))
+    # two slot sets: consecutive groups (also across steps) alternate, so the
+    # next group's stage 1 overlaps the previous group's binning + render
+    n_sets = (max(1, min(2, args.slot_sets)) if args.slot_sets > 0 else min(2, len(groups))) if groups else 0
     slots, pre_graphs, post_graphs, pre_streams = [], [], [], []
     if groups:
         slots = rasts[:G * n_sets] + [ab.Rasterizer(cfg["w"], cfg["h"], cfg["n"], device=dev, pair_capacity=rast.cap,
@@ -368,28 +375,31 @@ def run_ours(args, cfg, rank, world, local):
             torch.cuda.synchronize(dev)
             return g
 
-        post_graphs = [None] * n_mine
-        for gi, grp in enumerate(groups):
-            sl = [slots[(gi % n_sets) * G + q] for q in range(len(grp))]
-            gc = [cams[mine[j]] for j in grp]
-            before_b = L.adr_kernel_launches()
-            ab.render_views_batched(ds, gc, sl, mode=cfg["mode"])   # eager run before capture
-            torch.cuda.synchronize(dev)
-            if gi == 0:
-                launches_per_frame = (L.adr_kernel_launches() - before_b) / len(grp)
-            for r_ in sl:
-                assert not r_.truncated()
-            pre_graphs.append(capture(lambda cs, gc=gc, sl=sl: ab.preprocess_views(ds, gc, sl, mode=cfg["mode"],
-                                                                                   stream=cs)))
-            for q, j in enumerate(grp):
-                post_graphs[j] = capture(lambda cs, r_=sl[q], c_=gc[q]: r_.launch_post(ds, c_, mode=cfg["mode"],
-                                                                                       stream=cs))
+        # pre_graphs[set][group], post_graphs[set][view j of this rank]
+        pre_graphs = [[None] * len(groups) for _ in range(n_sets)]
+        post_graphs = [[None] * n_mine for _ in range(n_sets)]
+        for ss in range(n_sets):
+            for gi, grp in enumerate(groups):
+                sl = [slots[ss * G + q] for q in range(len(grp))]
+                gc = [cams[mine[j]] for j in grp]
+                before_b = L.adr_kernel_launches()
+                ab.render_views_batched(ds, gc, sl, mode=cfg["mode"])   # eager run before capture
+                torch.cuda.synchronize(dev)
+                if gi == 0 and ss == 0:
+                    launches_per_frame = (L.adr_kernel_launches() - before_b) / len(grp)
+                for r_ in sl:
+                    assert not r_.truncated()
+                pre_graphs[ss][gi] = capture(lambda cs, gc=gc, sl=sl: ab.preprocess_views(
+                    ds, gc, sl, mode=cfg["mode"], stream=cs))
+                for q, j in enumerate(grp):
+                    post_graphs[ss][j] = capture(lambda cs, r_=sl[q], c_=gc[q]: r_.launch_post(
+                        ds, c_, mode=cfg["mode"], stream=cs))
     fg = FrameGather(views, cfg["h"], cfg["w"], dev) if world > 1 else None
     zero = torch.zeros(1, dtype=torch.int64, device=dev)
     setup_s = time.perf_counter() - t_setup
     stream = torch.cuda.current_stream(dev)
 
-    def step(gather: bool):
+    def step(gather: bool, join: bool = True):
         """One batch: this rank's views (frames of different views overlap on
         the slot streams); with `gather`, each frame is shipped to rank 0 as
         soon as it is rendered and the step ends when every transfer landed."""
@@ -419,30 +429,35 @@ def run_ours(args, cfg, rank, world, local):
         for _ in range(7):
             q0, q1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
             q0.record(stream)
-            pre_graphs[0].replay()
+            pre_graphs[0][0].replay()
             q1.record(stream)
             torch.cuda.synchronize(dev)
             ts.append(q0.elapsed_time(q1))
         bpre_ms = statistics.median(ts[2:])
 
-    def step_batched(gather: bool):
+    gcount = [0]                                # groups issued so far (slot-set alternation)
+    pending = [[] for _ in range(n_sets)]       # per slot set: events of its last group's frames
+
+    def step_batched(gather: bool, join: bool = True):
         """One batch through batched stage 1: per group of G views one
-        preprocess_views graph on its slot set's stream, then each view's
-        stages 2-6 graph on the in-flight streams (gathered like `step`)."""
+        preprocess_views graph on its slot set's stream (waiting only for that
+        set's previous frames), then each view's stages 2-6 graph on the
+        in-flight streams (gathered like `step`).  Without `join` the next
+        step's stage 1 may start while this step's last frames still run."""
         ev0 = torch.cuda.Event()
         ev0.record(stream)
         for st in streams + pre_streams:
             st.wait_event(ev0)
         if fg is not None and gather:
             fg.begin()
-        pending = [[] for _ in range(n_sets)]
         for gi, grp in enumerate(groups):
-            ss = gi % n_sets
+            ss = gcount[0] % n_sets
+            gcount[0] += 1
             ps = pre_streams[ss]
             for e in pending[ss]:
                 ps.wait_event(e)
             with torch.cuda.stream(ps):
-                pre_graphs[gi].replay()
+                pre_graphs[ss][gi].replay()
             pe = torch.cuda.Event()
             pe.record(ps)
             used = []
@@ -450,7 +465,7 @@ def run_ours(args, cfg, rank, world, local):
                 k = j % n_fly
                 streams[k].wait_event(pe)
                 with torch.cuda.stream(streams[k]):
-                    post_graphs[j].replay()
+                    post_graphs[ss][j].replay()
                     if fg is not None and gather:
                         r = slots[ss * G + q]
                         fg.send(mine[j], r.pixels, r.load, torch.cat([r.counters[0:2], r.stats[0:3], zero]))
@@ -461,10 +476,11 @@ def run_ours(args, cfg, rank, world, local):
                 e = torch.cuda.Event()
                 e.record(streams[k])
                 pending[ss].append(e)
-        for st in streams + pre_streams:
-            ev = torch.cuda.Event()
-            ev.record(st)
-            stream.wait_event(ev)
+        if join or (fg is not None and gather):
+            for st in streams + pre_streams:
+                ev = torch.cuda.Event()
+                ev.record(st)
+                stream.wait_event(ev)
         if fg is not None and gather:
             fg.finish()
 
@@ -478,8 +494,8 @@ def run_ours(args, cfg, rank, world, local):
         torch.cuda.synchronize(dev)
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         e0.record(stream)
-        for _ in range(k_steps):
-            step(gather)
+        for i in range(k_steps):   # consecutive steps may overlap; the last one joins every stream
+            step(gather, join=(i == k_steps - 1))
         e1.record(stream)
         torch.cuda.synchronize(dev)
         ms = e0.elapsed_time(e1)
