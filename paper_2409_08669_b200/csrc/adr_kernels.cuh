@@ -39,6 +39,9 @@ struct __align__(16) Record {
 // fused preprocess derives it from the extent's ln(sigma / alpha_low) plus a
 // per-frame constant, within ~1e-7 — inside the 1e-5 margin, which is
 // widened by 2e-7 on that path); >= 1e300: computed here.
+#ifndef ADR_CULL_FAST
+#define ADR_CULL_FAST 1
+#endif
 __device__ inline void cull_params(float a, float b, float c, float op, float alpha_low32, float c0, float c1,
                                    float c2, float* tau, float* hx, float* hy,
                                    double ln_a_over_op = 1e300) {
@@ -52,14 +55,28 @@ __device__ inline void cull_params(float a, float b, float c, float op, float al
     *hx = *hy = kInf;
     if (!(op < 1e30f) || !isfinite(c0) || !isfinite(c1) || !isfinite(c2)) return;
     const double da = a, db = b, dc = c;
-    const double det = da * dc - db * db;
+    const double det = da * dc - db * db;   // fp64: no cancellation loss for near-singular conics
     if (!(det > 0.0) || !(da > 0.0) || !(dc > 0.0)) return;
+#if ADR_CULL_FAST
+    // The bounds below need not be correctly rounded, only conservative: they
+    // are evaluated in fp32 (a few ulp each) and every result that must not
+    // be too small is enlarged by a relative 1e-5 / 2e-6 that covers those
+    // errors many times over; the 1 + 1e-4 slack of s is left intact.
+    const float det32 = (float)det;
+    if (!(det32 > 0.0f)) return;   // fp32 underflow: slow splat (no culling)
+    const float dh = 0.5f * (a - c);
+    const float lmin = det32 / (0.5f * (a + c) + sqrtf(dh * dh + b * b));   // det / lambda_max
+    if (!(lmin > 0.0f)) return;
+    const float eta = (16.0f * 5.9604644775390625e-08f) * ((fmaxf(a, c) + 0.5f * fabsf(b)) / lmin) * 1.00001f;
+    if (!(eta < 0.25f)) return;
+#else
     const double half = 0.5 * (da + dc), rad = sqrt(0.25 * (da - dc) * (da - dc) + db * db);
     const double lmin = half - rad;
     if (!(lmin > 0.0)) return;
     const double M = (da > dc ? da : dc) + 0.5 * fabs(db);
     const double eta = 2.0 * 8.0 * 5.9604644775390625e-08 * M / lmin;
     if (!(eta < 0.25)) return;
+#endif
     const double t = ln_a_over_op < 1e299 ? ln_a_over_op - 1.02e-5
                                                   : log((double)alpha_low32 / (double)op) - 1e-5;
     float t32 = __double2float_rd(t);
@@ -70,9 +87,16 @@ __device__ inline void cull_params(float a, float b, float c, float op, float al
         *hx = *hy = 1.0f;
         return;
     }
+#if ADR_CULL_FAST
+    const float s = sqrtf((1.0f + 1e-4f) / (1.0f - eta)) * 1.000002f;
+    const float k_det = (float)K / det32;
+    *hx = __fadd_ru(s * sqrtf(k_det * c), 1e-3f);
+    *hy = __fadd_ru(s * sqrtf(k_det * a), 1e-3f);
+#else
     const double s = sqrt((1.0 + 1e-4) / (1.0 - eta));
     *hx = __double2float_ru(s * sqrt(K * dc / det) + 1e-3);
     *hy = __double2float_ru(s * sqrt(K * da / det) + 1e-3);
+#endif
 }
 
 // Extra per-Gaussian outputs the fused frame needs from stage 1.
