@@ -284,7 +284,8 @@ int32_t adr_preprocess_views(const adr_scene* scene, const adr_camera* cams, int
         int32_t rc = frame_setup(scene, &cams[v], alpha_low, &bufs[v], &f);
         if (rc) return rc;
         for (int u = 0; u < v; ++u)
-            if (bufs[u].d_scratch == bufs[v].d_scratch || bufs[u].d_counters == bufs[v].d_counters)
+            if (bufs[u].d_scratch == bufs[v].d_scratch || bufs[u].d_counters == bufs[v].d_counters ||
+                bufs[u].proj.d_valid == bufs[v].proj.d_valid)
                 return fail(ADR_ERR_VALUE, "preprocess_views: every view needs its own frame buffers");
         ADR_CUDA_TRY(cudaMemsetAsync(bufs[v].d_counters, 0, 8 * sizeof(int64_t), st));
         pv.cam[v] = cams[v];
