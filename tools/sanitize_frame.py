@@ -27,6 +27,11 @@ def main():
         ref_img, _ = ab.render_reference(ds, cam)
         torch.cuda.synchronize()
         assert torch.equal(ref_img.pixels.view(torch.int32), res.image.pixels.view(torch.int32))
+        cam2 = ab.Camera.from_lookat((-1.2, 0.4, -2.3), (0, 0, 0), width=640, height=360)
+        rasts = [ab.Rasterizer(640, 360, n, pair_capacity=2 * res.stats.pair_count + 4096) for _ in range(2)]
+        ab.render_views_batched(ds, [cam, cam2], rasts, mode="aabb")   # batched stage 1, multi-block
+        torch.cuda.synchronize()
+        assert torch.equal(rasts[0].pixels.view(torch.int32), res.image.pixels.view(torch.int32))
         print("sanitize frame OK", n, "Gaussians", res.stats.pair_count, "pairs")
         return
     a = ab.synthetic_arrays(5, 4000, spec, sh_degree=3, float32=True)
@@ -42,6 +47,16 @@ def main():
     rast = ab.Rasterizer(200, 136, len(ds), pair_capacity=500)   # overflow + regrow path
     rast.render(ds, cam)
     torch.cuda.synchronize()
+    # batched stage 1 (adr_preprocess_views + adr_render_frame_post): 3 views, one of them
+    # with a too-small pair capacity (truncated frame, no out-of-bounds writes)
+    cams = [cam, ab.Camera.from_lookat((-1.0, 0.5, -2.2), (0, 0, 0), width=200, height=136),
+            ab.Camera.from_lookat((1.5, 0.0, -2.0), (0, 0, 0), width=160, height=120)]
+    caps = [res.stats.pair_count + 64, 4 * res.stats.pair_count, 100]
+    rasts = [ab.Rasterizer(c.width, c.height, len(ds), pair_capacity=k) for c, k in zip(cams, caps)]
+    ab.render_views_batched(ds, cams, rasts, mode="aabb")
+    torch.cuda.synchronize()
+    assert torch.equal(rasts[0].pixels.view(torch.int32), res.image.pixels.view(torch.int32))
+    assert rasts[2].truncated() and not rasts[1].truncated()
     assert torch.equal(ref_img.pixels.view(torch.int32), res.image.pixels.view(torch.int32))
     print("sanitize frame OK", res.stats.pair_count, "pairs")
 
