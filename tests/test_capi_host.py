@@ -147,3 +147,21 @@ def test_product_path_has_no_cpu_fallback(monkeypatch, tmp_path):
     monkeypatch.setattr(_lib, "LIB_PATH", tmp_path / "missing.so")
     with pytest.raises(RuntimeError, match="no CPU fallback"):
         _lib.lib()
+
+
+def test_preprocess_views_host_validation():
+    """Host-side checks of the batched stage-1 call run before any CUDA work:
+    1..8 views, one distinct Rasterizer per view."""
+    import paper_2409_08669_b200 as ab
+
+    assert ab.MAX_BATCH_VIEWS == 8
+    cams, slots = [object()] * 9, [object() for _ in range(9)]
+    with pytest.raises(ValueError, match="1..8"):
+        ab.preprocess_views(None, cams, slots)
+    with pytest.raises(ValueError, match="1..8"):
+        ab.preprocess_views(None, [], [])
+    with pytest.raises(ValueError, match="one Rasterizer per view"):
+        ab.preprocess_views(None, cams[:3], slots[:2])
+    same = object()
+    with pytest.raises(ValueError, match="its own Rasterizer"):
+        ab.preprocess_views(None, cams[:2], [same, same])
