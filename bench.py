@@ -731,7 +731,11 @@ def run_ours(args, cfg, rank, world, local):
                 "achieved": (n * (44 + 12 * k_sh) + len(groups[0]) * n * 52) / (bpre_ms * 1e-3) / 1e9,
                 "frac": (n * (44 + 12 * k_sh) + len(groups[0]) * n * 52) / (bpre_ms * 1e-3) / 1e9 / hbm,
                 "per_view_equivalent_gbs": pre_bytes * len(groups[0]) / (bpre_ms * 1e-3) / 1e9,
-                "duration_source": "median of CUDA events around the group-0 stage-1 graph replayed alone"},
+                "duration_source": "median of CUDA events around the group-0 stage-1 graph replayed alone",
+                "bound": "fp64-issue",
+                "traffic": ncu.get("k_preprocess_views_dram_bytes"),
+                "issue_active": ncu.get("k_preprocess_views_issue_active"),
+                "fp64_pipe_active": ncu.get("k_preprocess_views_fp64_pipe")},
             "binning_roofline": {"bound": "hbm", "kernels": "depth sort + supertile items + pair placement",
                                  "bytes_per_frame": bin_bytes,
                                  "bytes_rule": "SURVEY.md §8(d): N·16 dup read + P·12 pair write + P·24 one ideal sort pass",

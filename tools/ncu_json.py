@@ -22,19 +22,23 @@ def launches(path):
     ki, mi, vi, ui = (hdr.index(x) for x in ("Kernel Name", "Metric Name", "Metric Value", "Metric Unit"))
     out = {}
     for r in data:
-        name = "k_render" if "k_render<" in r[ki] else ("k_preprocess" if "k_preprocess<" in r[ki] else None)
+        name = ("k_render" if "k_render<" in r[ki] else "k_preprocess" if "k_preprocess<" in r[ki]
+                else "k_preprocess_views" if "k_preprocess_views<" in r[ki] else None)
         if name and r[mi].startswith("dram__bytes"):
             out[name] = out.get(name, 0.0) + float(r[vi].replace(",", "")) * SCALE.get(r[ui], 1.0)
     return out
 
 
-def main(config, csv_path, rep=None):
+def main(config, csv_path, rep=None, batch_csv=None):
     d = json.loads(OUT.read_text()) if OUT.exists() else {}
     b = launches(csv_path)
     e = d.setdefault(config, {})
     e["k_render_dram_bytes"] = b.get("k_render")
     e["k_preprocess_dram_bytes"] = b.get("k_preprocess")
     e["source"] = str(csv_path)
+    if batch_csv:   # launch list of one batched step: the stage-1 launch's DRAM bytes
+        e["k_preprocess_views_dram_bytes"] = launches(batch_csv).get("k_preprocess_views")
+        e["batch_source"] = str(batch_csv)
     if rep:
         ms = ["sm__pipe_fma_cycles_active.avg.pct_of_peak_sustained_active",
               "smsp__issue_active.avg.pct_of_peak_sustained_active", "smsp__inst_executed.sum",
@@ -49,6 +53,15 @@ def main(config, csv_path, rep=None):
         e["k_render_issue_active"] = val[ms[1]] / 100.0
         # warp instructions issued per second (peak: 148 SMs x 4 schedulers x 1 / clock)
         e["k_render_warp_inst_per_s"] = val[ms[2]] / dur_s
+        pm = ["smsp__issue_active.avg.pct_of_peak_sustained_active",
+              "sm__pipe_fp64_cycles_active.avg.pct_of_peak_sustained_active"]
+        txt = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv", "--kernel-name",
+                              "regex:k_preprocess_views", "--metrics", ",".join(pm)],
+                             capture_output=True, text=True).stdout
+        rows = list(csv.reader(io.StringIO(txt)))
+        if len(rows) > 2:
+            e["k_preprocess_views_issue_active"] = float(rows[2][rows[0].index(pm[0])]) / 100.0
+            e["k_preprocess_views_fp64_pipe"] = float(rows[2][rows[0].index(pm[1])]) / 100.0
     OUT.write_text(json.dumps(d, indent=1) + "\n")
     print(json.dumps(d, indent=1))
 
