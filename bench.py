@@ -730,7 +730,6 @@ def run_ours(args, cfg, rank, world, local):
                 "bytes_rule": "SURVEY.md §8(d) with the scene read once per launch: N(44+12K) + views·52N",
                 "achieved": (n * (44 + 12 * k_sh) + len(groups[0]) * n * 52) / (bpre_ms * 1e-3) / 1e9,
                 "frac": (n * (44 + 12 * k_sh) + len(groups[0]) * n * 52) / (bpre_ms * 1e-3) / 1e9 / hbm,
-                "per_view_equivalent_gbs": pre_bytes * len(groups[0]) / (bpre_ms * 1e-3) / 1e9,
                 "duration_source": "median of CUDA events around the group-0 stage-1 graph replayed alone",
                 "bound": "fp64-issue",
                 "traffic": ncu.get("k_preprocess_views_dram_bytes"),
